@@ -1,0 +1,143 @@
+/*
+ * prng_b200.h -- C ABI of the B200-native RNG hot path (libprng_b200.so).
+ *
+ * Drop-in for the portarng kernel plugin (reference seam
+ * pkg/src/portarng/_kernels/__init__.py:10-27) and for the fused
+ * generate -> transform cycle the reference runs as two passes
+ * (rngburn.py:62-151, distributions.py:83-153).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no allocation on the device entry points,
+ *    no host synchronisation, stream-ordered on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream).  The device is taken from `out`.
+ *  - `out` is caller-owned device memory (or mapped pinned host memory),
+ *    aligned to its element size.
+ *  - Philox state arguments are exactly those of the reference kernel
+ *    philox_fill(k0, k1, b0, b1, b2, b3, offset, n) (_core.pyx:42):
+ *    key (k0, k1), 128-bit block counter ctr[0..3] (lane 0 least
+ *    significant) and `lane` = words of that block already consumed (0..3).
+ *    From an engine state at stream position p: ctr = p >> 2, lane = p & 3
+ *    (engine.py:221-225).
+ *  - MRG32k3a state arguments are the two recurrence windows s1[3], s2[3]
+ *    (Mrg32k3aState, engine.py:75-80), components < m1 / m2, not all zero.
+ *  - Return 0 on success or a negative PRNG_ERR_* code; prng_last_error()
+ *    returns the message for the calling thread.
+ *  - The word stream consumed by a request is the reference's: n words for
+ *    bits/uniform, 2*ceil(n/2) for gaussian/lognormal (fill_gaussian,
+ *    distributions.py:146-149), pairs taken relative to the request start.
+ */
+#ifndef PRNG_B200_H
+#define PRNG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRNG_ABI_VERSION 1
+
+/* Status codes: 1:1 with the reference exception types (errors.py). */
+#define PRNG_OK 0
+#define PRNG_ERR_UNSUPPORTED_ENGINE (-1) /* errors.py:8  UnsupportedEngine */
+#define PRNG_ERR_INVALID_RANGE (-2)      /* errors.py:12 InvalidRange      */
+#define PRNG_ERR_INVALID_PARAMETER (-3)  /* errors.py:16 InvalidParameter  */
+#define PRNG_ERR_VALUE (-4)              /* ValueError (engine.py:206,219) */
+#define PRNG_ERR_CUDA (-5)               /* CUDA runtime failure           */
+
+/* Gaussian / lognormal fp32 method.  FAST: fp32 logf/sqrtf/sincospif
+ * (documented tolerance).  ACCURATE: the reference's
+ * fp64 formula, then cast (fp64 outputs always use ACCURATE). */
+#define PRNG_METHOD_FAST 0
+#define PRNG_METHOD_ACCURATE 1
+
+int prng_abi_version(void);
+const char *prng_last_error(void);
+
+/* ---- Philox4x32-10: replaces _core.philox_fill (_core.pyx:42-71) + the
+ *      words_to_unit / range_transform / Box-Muller passes. ---- */
+
+/* uniform_bits uint32: engine.generate_words (engine.py:212-226) */
+int prng_philox4x32x10_bits(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                            uint32_t *out, void *stream);
+/* uniform on [a, b): fill_uniform_unit + range_transform (distributions.py:90-104) */
+int prng_philox4x32x10_uniform_f32(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                   double a, double b, float *out, void *stream);
+int prng_philox4x32x10_uniform_f64(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                   double a, double b, double *out, void *stream);
+/* gaussian: fill_gaussian (distributions.py:134-153) */
+int prng_philox4x32x10_gaussian_f32(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                    double mean, double stddev, int method, float *out, void *stream);
+int prng_philox4x32x10_gaussian_f64(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                    double mean, double stddev, double *out, void *stream);
+/* lognormal (extension; oneMKL lognormal(m, s, displ, scale)) */
+int prng_philox4x32x10_lognormal_f32(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                     double m, double s, double displ, double scale, int method, float *out,
+                                     void *stream);
+int prng_philox4x32x10_lognormal_f64(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
+                                     double m, double s, double displ, double scale, double *out, void *stream);
+
+/* ---- MRG32k3a: replaces _core.mrg_fill (_core.pyx:74-102), split across
+ *      threads by jump-ahead.  The caller advances its state with
+ *      prng_mrg32k3a_skip_ahead(s, n) (or 2*ceil(n/2) for pair dists). ---- */
+int prng_mrg32k3a_bits(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, uint32_t *out, void *stream);
+int prng_mrg32k3a_uniform_f32(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double a, double b,
+                              float *out, void *stream);
+int prng_mrg32k3a_uniform_f64(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double a, double b,
+                              double *out, void *stream);
+int prng_mrg32k3a_gaussian_f32(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double mean,
+                               double stddev, int method, float *out, void *stream);
+int prng_mrg32k3a_gaussian_f64(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double mean,
+                               double stddev, double *out, void *stream);
+int prng_mrg32k3a_lognormal_f32(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double m, double s,
+                                double displ, double scale, int method, float *out, void *stream);
+int prng_mrg32k3a_lognormal_f64(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double m, double s,
+                                double displ, double scale, double *out, void *stream);
+
+/* MRG32k3a jump-ahead by k = k_hi * 2^64 + k_lo words (host only; absent in
+ * the reference, engine.py:201-202).  s*_out may alias s*. */
+int prng_mrg32k3a_skip_ahead(const uint32_t s1[3], const uint32_t s2[3], uint64_t k_lo, uint64_t k_hi,
+                             uint32_t s1_out[3], uint32_t s2_out[3]);
+
+/* In-place affine range transform of unit values (distributions.py:98-104),
+ * same two-rounding arithmetic as the fused path. */
+int prng_range_transform_f32(float *values, uint64_t n, double lo, double hi, void *stream);
+int prng_range_transform_f64(double *values, uint64_t n, double lo, double hi, void *stream);
+
+/* Word-array transforms (distributions.py:83-87, 116-131) on device arrays:
+ * words_to_unit maps n words; gaussian_from_words reads 2*ceil(n/2) words. */
+int prng_words_to_unit_f32(const uint32_t *words, uint64_t n, float *out, void *stream);
+int prng_words_to_unit_f64(const uint32_t *words, uint64_t n, double *out, void *stream);
+int prng_gaussian_from_words_f32(const uint32_t *words, uint64_t n, double mean, double stddev, int method,
+                                 float *out, void *stream);
+int prng_gaussian_from_words_f64(const uint32_t *words, uint64_t n, double mean, double stddev, double *out,
+                                 void *stream);
+
+/* ---- Many small batches (FastCaloSim consumer, calosim.py:269-358). ----
+ * One launch generates every segment: segment i writes `count` fp32 uniforms
+ * on [a, b) of the Philox stream starting at 128-bit word position
+ * (pos_hi:pos_lo) to out + out_offset.  `segs` is device memory. */
+typedef struct prng_segment {
+    uint64_t pos_lo, pos_hi;
+    uint64_t count;
+    uint64_t out_offset;
+} prng_segment_t;
+int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng_segment_t *segs, uint32_t nseg,
+                                            uint64_t max_count, double a, double b, float *out, void *stream);
+
+/* ---- Host-buffer drop-ins for the reference kernel plugin
+ *      (portarng._kernels: philox_fill / mrg_fill / box_muller,
+ *      _kernels/__init__.py:24-27).  Synchronous; generate on the current
+ *      device into library-owned scratch and copy to the host buffer. ---- */
+int prng_kernels_philox_fill(uint32_t k0, uint32_t k1, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                             uint32_t offset, uint64_t n, uint32_t *host_out);
+int prng_kernels_mrg_fill(uint32_t s10, uint32_t s11, uint32_t s12, uint32_t s20, uint32_t s21, uint32_t s22,
+                          uint64_t n, uint32_t *host_out, uint32_t s1_out[3], uint32_t s2_out[3]);
+int prng_kernels_box_muller(const double *u1, const double *u2, uint64_t m, double *z0, double *z1);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRNG_B200_H */

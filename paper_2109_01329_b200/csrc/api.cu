@@ -1,0 +1,761 @@
+// api.cu -- extern "C" boundary of libprng_b200.so (include/prng_b200.h).
+//
+// Host-side validation mirrors the reference's error behaviour
+// (distributions.py:47-48, 60-62, 100-101; engine.py:206, 219); the launch
+// planners pick the kernel instantiation and grid.  No entry point on the
+// device path allocates memory or synchronises the host.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "../../include/prng_b200.h"
+#include "common.cuh"
+#include "mrg32k3a.cuh"
+#include "philox.cuh"
+
+using namespace prng;
+
+static_assert(sizeof(prng_segment_t) == sizeof(PhiloxSegment), "segment layout");
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(PRNG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define PRNG_CUDA(call)                                     \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// ---- device resolution: the device that owns `ptr` becomes current ----
+int bind_output(const void* ptr, void** dev_ptr) {
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(e, "cudaPointerGetAttributes(out)");
+    }
+    if (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) {
+        int cur = -1;
+        PRNG_CUDA(cudaGetDevice(&cur));
+        if (cur != attr.device) PRNG_CUDA(cudaSetDevice(attr.device));
+        *dev_ptr = const_cast<void*>(ptr);
+        return PRNG_OK;
+    }
+    if (attr.type == cudaMemoryTypeHost && attr.devicePointer != nullptr) {
+        *dev_ptr = attr.devicePointer;  // mapped pinned host memory (zero-copy)
+        return PRNG_OK;
+    }
+    return fail(PRNG_ERR_INVALID_PARAMETER, "out must be device memory or mapped pinned host memory");
+}
+
+struct DeviceInfo {
+    int sms = 0;
+    std::map<const void*, int> occ;
+};
+std::mutex g_mu;
+std::map<int, DeviceInfo> g_dev;
+
+int resident_ctas(const void* kernel, int threads, int* sms_out, int* occ_out) {
+    int dev = 0;
+    PRNG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceInfo& di = g_dev[dev];
+    if (di.sms == 0) PRNG_CUDA(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+    auto it = di.occ.find(kernel);
+    if (it == di.occ.end()) {
+        int o = 0;
+        PRNG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, 0));
+        it = di.occ.emplace(kernel, o < 1 ? 1 : o).first;
+    }
+    *sms_out = di.sms;
+    *occ_out = it->second;
+    return PRNG_OK;
+}
+
+// ---- parameter validation (reference error behaviour) ----
+int check_uniform(double a, double b) {
+    if (!(std::isfinite(a) && std::isfinite(b)) || a >= b)
+        return fail(PRNG_ERR_INVALID_RANGE, "uniform range requires finite lo < hi, got [%g, %g)", a, b);
+    return PRNG_OK;
+}
+
+int check_gaussian(double mean, double sd) {
+    if (!std::isfinite(mean) || !std::isfinite(sd) || sd <= 0)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "gaussian requires finite mean and stddev > 0, got (%g, %g)", mean,
+                    sd);
+    return PRNG_OK;
+}
+
+int check_lognormal(double m, double s, double displ, double scale) {
+    if (!std::isfinite(m) || !std::isfinite(s) || s <= 0 || !std::isfinite(displ) || !std::isfinite(scale) ||
+        scale <= 0)
+        return fail(PRNG_ERR_INVALID_PARAMETER,
+                    "lognormal requires finite m, s > 0, finite displ, scale > 0, got (%g, %g, %g, %g)", m, s, displ,
+                    scale);
+    return PRNG_OK;
+}
+
+int check_method(int method) {
+    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST or PRNG_METHOD_ACCURATE");
+    return PRNG_OK;
+}
+
+// Uniform [a, b) plan.  numpy NEP-50 makes the fp32 affine use f32(b - a)
+// and f32(a) (distributions.py:102-103 on an fp32 array); fp64 uses b - a, a.
+enum UniformPlan { kPlanIdentity, kPlanFolded, kPlanTwoPass };
+
+struct UniformSpec {
+    UniformPlan plan;
+    XformParams p;
+};
+
+UniformSpec uniform_spec_f32(double a, double b) {
+    UniformSpec u{};
+    const float S = (float)(b - a), off = (float)a;
+    u.p.scale_f = S * 5.9604644775390625e-08f;  // exact power-of-two scaling when normal
+    u.p.off_f = off;
+    if (S == 1.0f && off == 0.0f)
+        u.plan = kPlanIdentity;
+    else if (std::isinf(S) || S >= 0x1p-102f)
+        u.plan = kPlanFolded;
+    else
+        u.plan = kPlanTwoPass;
+    return u;
+}
+
+UniformSpec uniform_spec_f64(double a, double b) {
+    UniformSpec u{};
+    const double S = b - a;
+    u.p.scale_d = S * 5.9604644775390625e-08;
+    u.p.off_d = a;
+    if (S == 1.0 && a == 0.0)
+        u.plan = kPlanIdentity;
+    else if (std::isinf(S) || S >= 0x1p-998)
+        u.plan = kPlanFolded;
+    else
+        u.plan = kPlanTwoPass;
+    return u;
+}
+
+XformParams gauss_params(double mean, double sd) {
+    XformParams p{};
+    p.scale_f = (float)sd;
+    p.off_f = (float)mean;
+    p.scale_d = sd;
+    p.off_d = mean;
+    return p;
+}
+
+XformParams logn_params(double m, double s, double displ, double scale) {
+    XformParams p = gauss_params(m, s);
+    p.ln_scale = scale;
+    p.ln_displ = displ;
+    p.ln_scale_f = (float)scale;
+    p.ln_displ_f = (float)displ;
+    return p;
+}
+
+template <typename T>
+int launch_range(T* v, uint64_t n, double lo, double hi, void* stream);
+
+// ---- Philox launch ----
+template <int X>
+int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, uint64_t n, void* out,
+                  const XformParams& p, void* stream) {
+    using T = typename XformTraits<X>::T;
+    if (n == 0) return PRNG_OK;
+    if (ctr == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "ctr must not be NULL");
+    if (lane > 3) return fail(PRNG_ERR_INVALID_PARAMETER, "lane must be 0..3, got %u", lane);
+    if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+    if (((uintptr_t)out) % sizeof(T)) return fail(PRNG_ERR_INVALID_PARAMETER, "out is not aligned to its element");
+    void* dptr = nullptr;
+    int rc = bind_output(out, &dptr);
+    if (rc) return rc;
+
+    PhiloxLaunch a{};
+    a.k0 = k0;
+    a.k1 = k1;
+    a.ctr_lo = (uint64_t)ctr[0] | ((uint64_t)ctr[1] << 32);
+    a.ctr_hi = (uint64_t)ctr[2] | ((uint64_t)ctr[3] << 32);
+    a.lane = lane;
+    a.n = n;
+    a.out = dptr;
+    a.p = p;
+    const int shift = plan_philox(a, (uint64_t)(uintptr_t)dptr, sizeof(T), XformTraits<X>::kPair);
+
+    const void* kern;
+    uint64_t threads;
+    switch (shift) {
+        case 0:
+            kern = (const void*)philox_kernel<X, 0>;
+            threads = sizeof(T) == 4 ? (a.ngroups + 1) / 2 : a.ngroups;
+            break;
+        case 1: kern = (const void*)philox_kernel<X, 1>; threads = (a.ngroups + 30) / 31 * 32; break;
+        case 2: kern = (const void*)philox_kernel<X, 2>; threads = (a.ngroups + 30) / 31 * 32; break;
+        default: kern = (const void*)philox_kernel<X, 3>; threads = (a.ngroups + 30) / 31 * 32; break;
+    }
+    const uint64_t nscalar = a.i0 + (a.n - a.i0 - 4 * a.ngroups);
+    if (nscalar > threads) threads = nscalar;
+    int sms = 0, occ = 0;
+    rc = resident_ctas(kern, kPhiloxThreads, &sms, &occ);
+    if (rc) return rc;
+    uint64_t blocks = (threads + kPhiloxThreads - 1) / kPhiloxThreads;
+    const uint64_t cap = (uint64_t)sms * occ;
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    void* args[] = {&a};
+    PRNG_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(kPhiloxThreads), args, 0, (cudaStream_t)stream));
+    return PRNG_OK;
+}
+
+// ---- MRG32k3a host math: jump matrices A^k mod m ----
+typedef unsigned __int128 u128;
+struct Mat3 {
+    uint64_t v[9];
+};
+
+Mat3 mat_mul(const Mat3& a, const Mat3& b, uint64_t m) {
+    Mat3 r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            u128 s = 0;
+            for (int k = 0; k < 3; ++k) s += (u128)a.v[3 * i + k] * b.v[3 * k + j];
+            r.v[3 * i + j] = (uint64_t)(s % m);
+        }
+    return r;
+}
+
+void mat_vec(const Mat3& a, uint32_t* x, uint64_t m) {
+    uint64_t r[3];
+    for (int i = 0; i < 3; ++i) {
+        u128 s = 0;
+        for (int k = 0; k < 3; ++k) s += (u128)a.v[3 * i + k] * x[k];
+        r[i] = (uint64_t)(s % m);
+    }
+    for (int i = 0; i < 3; ++i) x[i] = (uint32_t)r[i];
+}
+
+// Companion matrices on (x_{n-3}, x_{n-2}, x_{n-1}) (engine.py:165-174).
+const Mat3 kA1 = {{0, 1, 0, 0, 0, 1, kMrgM1 - kMrgA13N, kMrgA12, 0}};
+const Mat3 kA2 = {{0, 1, 0, 0, 0, 1, kMrgM2 - kMrgA23N, 0, kMrgA21}};
+
+Mat3 mat_identity() { return Mat3{{1, 0, 0, 0, 1, 0, 0, 0, 1}}; }
+
+// A^(2^i) cache for i < 128 (shared by skip_ahead and the launch tables).
+struct PowCache {
+    std::vector<Mat3> p1, p2;
+    PowCache() {
+        Mat3 a = kA1, b = kA2;
+        for (int i = 0; i < 128; ++i) {
+            p1.push_back(a);
+            p2.push_back(b);
+            a = mat_mul(a, a, kMrgM1);
+            b = mat_mul(b, b, kMrgM2);
+        }
+    }
+};
+const PowCache& pow_cache() {
+    static PowCache c;
+    return c;
+}
+
+void mat_pow_u64(uint64_t k, Mat3* r1, Mat3* r2) {
+    const PowCache& c = pow_cache();
+    Mat3 a = mat_identity(), b = mat_identity();
+    for (int i = 0; i < 64; ++i)
+        if ((k >> i) & 1) {
+            a = mat_mul(a, c.p1[i], kMrgM1);
+            b = mat_mul(b, c.p2[i], kMrgM2);
+        }
+    *r1 = a;
+    *r2 = b;
+}
+
+int check_mrg_state(const uint32_t* s1, const uint32_t* s2) {
+    if (!s1 || !s2) return fail(PRNG_ERR_INVALID_PARAMETER, "MRG32k3a state must not be NULL");
+    for (int i = 0; i < 3; ++i)
+        if (s1[i] >= kMrgM1 || s2[i] >= kMrgM2)
+            return fail(PRNG_ERR_INVALID_PARAMETER, "MRG32k3a state components must be below their modulus");
+    if ((s1[0] | s1[1] | s1[2]) == 0 || (s2[0] | s2[1] | s2[2]) == 0)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "MRG32k3a state components must not be all zero");
+    return PRNG_OK;
+}
+
+struct MrgTables {
+    uint32_t nbits;
+    uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];
+};
+std::mutex g_mrg_mu;
+std::map<std::pair<uint64_t, uint32_t>, MrgTables> g_mrg_tables;
+
+const MrgTables& mrg_tables(uint64_t chunk, uint32_t nbits) {
+    std::lock_guard<std::mutex> lk(g_mrg_mu);
+    auto key = std::make_pair(chunk, nbits);
+    auto it = g_mrg_tables.find(key);
+    if (it != g_mrg_tables.end()) return it->second;
+    MrgTables t{};
+    t.nbits = nbits;
+    Mat3 a, b;
+    mat_pow_u64(chunk, &a, &b);
+    for (uint32_t i = 0; i < nbits; ++i) {
+        for (int e = 0; e < 9; ++e) {
+            t.j1[i][e] = (uint32_t)a.v[e];
+            t.j2[i][e] = (uint32_t)b.v[e];
+        }
+        a = mat_mul(a, a, kMrgM1);
+        b = mat_mul(b, b, kMrgM2);
+    }
+    if (g_mrg_tables.size() > 256) g_mrg_tables.clear();
+    return g_mrg_tables.emplace(key, t).first->second;
+}
+
+template <int X>
+int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, const XformParams& p, void* stream) {
+    using T = typename XformTraits<X>::T;
+    constexpr uint64_t TW = MrgTile<T>::kWords;
+    if (n == 0) return PRNG_OK;
+    int rc = check_mrg_state(s1, s2);
+    if (rc) return rc;
+    if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+    if (((uintptr_t)out) % sizeof(T)) return fail(PRNG_ERR_INVALID_PARAMETER, "out is not aligned to its element");
+    void* dptr = nullptr;
+    rc = bind_output(out, &dptr);
+    if (rc) return rc;
+    const void* kern = (const void*)mrg_kernel<X>;
+    int sms = 0, occ = 0;
+    rc = resident_ctas(kern, kMrgThreads, &sms, &occ);
+    if (rc) return rc;
+    const uint64_t tmax = (uint64_t)sms * occ * kMrgThreads;
+    uint64_t chunk = (n + tmax - 1) / tmax;
+    chunk = (chunk + TW - 1) / TW * TW;
+    const uint64_t tact = (n + chunk - 1) / chunk;
+    uint32_t nbits = 0;
+    while (nbits < 64 && ((tact - 1) >> nbits) != 0) ++nbits;
+    if (nbits > (uint32_t)kMrgMaxBits) return fail(PRNG_ERR_INVALID_PARAMETER, "request too large");
+    const MrgTables& tb = mrg_tables(chunk, nbits);
+    MrgLaunch a{};
+    for (int i = 0; i < 3; ++i) {
+        a.s1[i] = s1[i];
+        a.s2[i] = s2[i];
+    }
+    a.n = n;
+    a.chunk = chunk;
+    a.nbits = nbits;
+    memcpy(a.j1, tb.j1, sizeof a.j1);
+    memcpy(a.j2, tb.j2, sizeof a.j2);
+    a.out = dptr;
+    a.p = p;
+    const uint64_t blocks = (tact + kMrgThreads - 1) / kMrgThreads;
+    void* args[] = {&a};
+    PRNG_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(kMrgThreads), args, 0, (cudaStream_t)stream));
+    return PRNG_OK;
+}
+
+// ---- elementwise kernels ----
+template <typename T>
+__global__ void range_kernel(T* v, uint64_t n, T scale, T off) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if constexpr (sizeof(T) == 4)
+            v[i] = __fadd_rn(__fmul_rn(v[i], scale), off);
+        else
+            v[i] = __dadd_rn(__dmul_rn(v[i], scale), off);
+    }
+}
+
+__global__ void box_muller_kernel(const double* u1, const double* u2, uint64_t m, double* z0, double* z1) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        // _core.pyx:116-121 (u1 pre-flipped by the caller)
+        const double r = sqrt(__dmul_rn(-2.0, log(u1[i])));
+        const double t = __dmul_rn(kTwoPi, u2[i]);
+        double s, c;
+        sincos(t, &s, &c);
+        z0[i] = __dmul_rn(r, c);
+        z1[i] = __dmul_rn(r, s);
+    }
+}
+
+template <int X>
+__global__ void words_kernel(const uint32_t* __restrict__ w, uint64_t n, XformParams p,
+                             typename XformTraits<X>::T* __restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;; i += stride) {
+        if constexpr (XformTraits<X>::kPair) {
+            if (2 * i >= n) break;
+            typename XformTraits<X>::T o0, o1;
+            xform2<X>(w[2 * i], w[2 * i + 1], p, o0, o1);
+            out[2 * i] = o0;
+            if (2 * i + 1 < n) out[2 * i + 1] = o1;
+        } else {
+            if (i >= n) break;
+            out[i] = xform1<X>(w[i], p);
+        }
+    }
+}
+
+template <int X>
+int launch_words(const uint32_t* w, uint64_t n, const XformParams& p, void* out, void* stream) {
+    using T = typename XformTraits<X>::T;
+    if (n == 0) return PRNG_OK;
+    if (!w || !out) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL array");
+    if (((uintptr_t)out) % sizeof(T)) return fail(PRNG_ERR_INVALID_PARAMETER, "out is not aligned to its element");
+    void* d = nullptr;
+    int rc = bind_output(out, &d);
+    if (rc) return rc;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    words_kernel<X><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(w, n, p, (T*)d);
+    PRNG_CUDA(cudaGetLastError());
+    return PRNG_OK;
+}
+
+template <typename T>
+int launch_range(T* v, uint64_t n, double lo, double hi, void* stream) {
+    int rc = check_uniform(lo, hi);
+    if (rc) return rc;
+    if (n == 0) return PRNG_OK;
+    if (!v) return fail(PRNG_ERR_INVALID_PARAMETER, "values must not be NULL");
+    void* d = nullptr;
+    rc = bind_output(v, &d);
+    if (rc) return rc;
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    range_kernel<T><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((T*)d, n, (T)(hi - lo), (T)lo);
+    PRNG_CUDA(cudaGetLastError());
+    return PRNG_OK;
+}
+
+// ---- library-owned scratch for the host-buffer drop-ins ----
+struct Scratch {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    cudaStream_t stream = nullptr;
+};
+std::mutex g_scratch_mu;
+std::map<int, Scratch> g_scratch;
+
+int scratch(size_t bytes, void** p, cudaStream_t* s) {
+    int dev = 0;
+    PRNG_CUDA(cudaGetDevice(&dev));
+    Scratch& sc = g_scratch[dev];
+    if (!sc.stream) PRNG_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+    if (sc.bytes < bytes) {
+        if (sc.ptr) PRNG_CUDA(cudaFree(sc.ptr));
+        sc.ptr = nullptr;
+        sc.bytes = 0;
+        PRNG_CUDA(cudaMalloc(&sc.ptr, bytes));
+        sc.bytes = bytes;
+    }
+    *p = sc.ptr;
+    *s = sc.stream;
+    return PRNG_OK;
+}
+
+constexpr uint64_t kHostChunk = 1ull << 26;  // words per staged chunk
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int prng_abi_version(void) { return PRNG_ABI_VERSION; }
+const char* prng_last_error(void) { return g_err; }
+
+#define PHILOX_ARGS uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n
+
+int prng_philox4x32x10_bits(PHILOX_ARGS, uint32_t* out, void* stream) {
+    return launch_philox<kBits>(k0, k1, ctr, lane, n, out, XformParams{}, stream);
+}
+
+int prng_philox4x32x10_uniform_f32(PHILOX_ARGS, double a, double b, float* out, void* stream) {
+    int rc = check_uniform(a, b);
+    if (rc) return rc;
+    const UniformSpec u = uniform_spec_f32(a, b);
+    if (u.plan == kPlanFolded) return launch_philox<kUniformF32>(k0, k1, ctr, lane, n, out, u.p, stream);
+    rc = launch_philox<kUnitF32>(k0, k1, ctr, lane, n, out, u.p, stream);
+    return (rc || u.plan == kPlanIdentity) ? rc : launch_range<float>(out, n, a, b, stream);
+}
+
+int prng_philox4x32x10_uniform_f64(PHILOX_ARGS, double a, double b, double* out, void* stream) {
+    int rc = check_uniform(a, b);
+    if (rc) return rc;
+    const UniformSpec u = uniform_spec_f64(a, b);
+    if (u.plan == kPlanFolded) return launch_philox<kUniformF64>(k0, k1, ctr, lane, n, out, u.p, stream);
+    rc = launch_philox<kUnitF64>(k0, k1, ctr, lane, n, out, u.p, stream);
+    return (rc || u.plan == kPlanIdentity) ? rc : launch_range<double>(out, n, a, b, stream);
+}
+
+int prng_philox4x32x10_gaussian_f32(PHILOX_ARGS, double mean, double stddev, int method, float* out,
+                                    void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    if (!rc) rc = check_method(method);
+    if (rc) return rc;
+    const XformParams p = gauss_params(mean, stddev);
+    return method == PRNG_METHOD_FAST ? launch_philox<kGaussF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
+                                      : launch_philox<kGaussF32Accurate>(k0, k1, ctr, lane, n, out, p, stream);
+}
+
+int prng_philox4x32x10_gaussian_f64(PHILOX_ARGS, double mean, double stddev, double* out, void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    return rc ? rc : launch_philox<kGaussF64>(k0, k1, ctr, lane, n, out, gauss_params(mean, stddev), stream);
+}
+
+int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double displ, double scale, int method,
+                                     float* out, void* stream) {
+    int rc = check_lognormal(m, s, displ, scale);
+    if (!rc) rc = check_method(method);
+    if (rc) return rc;
+    const XformParams p = logn_params(m, s, displ, scale);
+    return method == PRNG_METHOD_FAST ? launch_philox<kLognF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
+                                      : launch_philox<kLognF32Accurate>(k0, k1, ctr, lane, n, out, p, stream);
+}
+
+int prng_philox4x32x10_lognormal_f64(PHILOX_ARGS, double m, double s, double displ, double scale, double* out,
+                                     void* stream) {
+    int rc = check_lognormal(m, s, displ, scale);
+    return rc ? rc
+              : launch_philox<kLognF64>(k0, k1, ctr, lane, n, out, logn_params(m, s, displ, scale), stream);
+}
+
+#define MRG_ARGS const uint32_t s1[3], const uint32_t s2[3], uint64_t n
+
+int prng_mrg32k3a_bits(MRG_ARGS, uint32_t* out, void* stream) {
+    return launch_mrg<kBits>(s1, s2, n, out, XformParams{}, stream);
+}
+
+int prng_mrg32k3a_uniform_f32(MRG_ARGS, double a, double b, float* out, void* stream) {
+    int rc = check_uniform(a, b);
+    if (rc) return rc;
+    const UniformSpec u = uniform_spec_f32(a, b);
+    if (u.plan == kPlanFolded) return launch_mrg<kUniformF32>(s1, s2, n, out, u.p, stream);
+    rc = launch_mrg<kUnitF32>(s1, s2, n, out, u.p, stream);
+    return (rc || u.plan == kPlanIdentity) ? rc : launch_range<float>(out, n, a, b, stream);
+}
+
+int prng_mrg32k3a_uniform_f64(MRG_ARGS, double a, double b, double* out, void* stream) {
+    int rc = check_uniform(a, b);
+    if (rc) return rc;
+    const UniformSpec u = uniform_spec_f64(a, b);
+    if (u.plan == kPlanFolded) return launch_mrg<kUniformF64>(s1, s2, n, out, u.p, stream);
+    rc = launch_mrg<kUnitF64>(s1, s2, n, out, u.p, stream);
+    return (rc || u.plan == kPlanIdentity) ? rc : launch_range<double>(out, n, a, b, stream);
+}
+
+int prng_mrg32k3a_gaussian_f32(MRG_ARGS, double mean, double stddev, int method, float* out, void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    if (!rc) rc = check_method(method);
+    if (rc) return rc;
+    const XformParams p = gauss_params(mean, stddev);
+    return method == PRNG_METHOD_FAST ? launch_mrg<kGaussF32Fast>(s1, s2, n, out, p, stream)
+                                      : launch_mrg<kGaussF32Accurate>(s1, s2, n, out, p, stream);
+}
+
+int prng_mrg32k3a_gaussian_f64(MRG_ARGS, double mean, double stddev, double* out, void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    return rc ? rc : launch_mrg<kGaussF64>(s1, s2, n, out, gauss_params(mean, stddev), stream);
+}
+
+int prng_mrg32k3a_lognormal_f32(MRG_ARGS, double m, double s, double displ, double scale, int method, float* out,
+                                void* stream) {
+    int rc = check_lognormal(m, s, displ, scale);
+    if (!rc) rc = check_method(method);
+    if (rc) return rc;
+    const XformParams p = logn_params(m, s, displ, scale);
+    return method == PRNG_METHOD_FAST ? launch_mrg<kLognF32Fast>(s1, s2, n, out, p, stream)
+                                      : launch_mrg<kLognF32Accurate>(s1, s2, n, out, p, stream);
+}
+
+int prng_mrg32k3a_lognormal_f64(MRG_ARGS, double m, double s, double displ, double scale, double* out,
+                                void* stream) {
+    int rc = check_lognormal(m, s, displ, scale);
+    return rc ? rc : launch_mrg<kLognF64>(s1, s2, n, out, logn_params(m, s, displ, scale), stream);
+}
+
+int prng_mrg32k3a_skip_ahead(const uint32_t s1[3], const uint32_t s2[3], uint64_t k_lo, uint64_t k_hi,
+                             uint32_t s1_out[3], uint32_t s2_out[3]) {
+    int rc = check_mrg_state(s1, s2);
+    if (rc) return rc;
+    if (!s1_out || !s2_out) return fail(PRNG_ERR_INVALID_PARAMETER, "output state must not be NULL");
+    uint32_t x1[3] = {s1[0], s1[1], s1[2]}, x2[3] = {s2[0], s2[1], s2[2]};
+    const PowCache& c = pow_cache();
+    for (int w = 0; w < 2; ++w) {
+        const uint64_t k = w ? k_hi : k_lo;
+        for (int i = 0; i < 64; ++i)
+            if ((k >> i) & 1) {
+                mat_vec(c.p1[64 * w + i], x1, kMrgM1);
+                mat_vec(c.p2[64 * w + i], x2, kMrgM2);
+            }
+    }
+    for (int i = 0; i < 3; ++i) {
+        s1_out[i] = x1[i];
+        s2_out[i] = x2[i];
+    }
+    return PRNG_OK;
+}
+
+int prng_words_to_unit_f32(const uint32_t* words, uint64_t n, float* out, void* stream) {
+    return launch_words<kUnitF32>(words, n, XformParams{}, out, stream);
+}
+
+int prng_words_to_unit_f64(const uint32_t* words, uint64_t n, double* out, void* stream) {
+    return launch_words<kUnitF64>(words, n, XformParams{}, out, stream);
+}
+
+int prng_gaussian_from_words_f32(const uint32_t* words, uint64_t n, double mean, double stddev, int method,
+                                 float* out, void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    if (!rc) rc = check_method(method);
+    if (rc) return rc;
+    const XformParams p = gauss_params(mean, stddev);
+    return method == PRNG_METHOD_FAST ? launch_words<kGaussF32Fast>(words, n, p, out, stream)
+                                      : launch_words<kGaussF32Accurate>(words, n, p, out, stream);
+}
+
+int prng_gaussian_from_words_f64(const uint32_t* words, uint64_t n, double mean, double stddev, double* out,
+                                 void* stream) {
+    int rc = check_gaussian(mean, stddev);
+    return rc ? rc : launch_words<kGaussF64>(words, n, gauss_params(mean, stddev), out, stream);
+}
+
+int prng_range_transform_f32(float* values, uint64_t n, double lo, double hi, void* stream) {
+    return launch_range<float>(values, n, lo, hi, stream);
+}
+
+int prng_range_transform_f64(double* values, uint64_t n, double lo, double hi, void* stream) {
+    return launch_range<double>(values, n, lo, hi, stream);
+}
+
+int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng_segment_t* segs, uint32_t nseg,
+                                            uint64_t max_count, double a, double b, float* out, void* stream) {
+    int rc = check_uniform(a, b);
+    if (rc) return rc;
+    if (nseg == 0 || max_count == 0) return PRNG_OK;
+    if (!segs || !out) return fail(PRNG_ERR_INVALID_PARAMETER, "segs and out must not be NULL");
+    if (((uintptr_t)out) % 4) return fail(PRNG_ERR_INVALID_PARAMETER, "out is not aligned to its element");
+    void* dptr = nullptr;
+    rc = bind_output(out, &dptr);
+    if (rc) return rc;
+    const void* kern = (const void*)philox_segments_kernel<kUniformF32>;
+    int sms = 0, occ = 0;
+    rc = resident_ctas(kern, kPhiloxThreads, &sms, &occ);
+    if (rc) return rc;
+    // blocks per segment: enough threads for 8 elements each, but keep the
+    // whole grid within ~4 waves of resident CTAs.
+    uint64_t bx = (max_count / 8 + kPhiloxThreads) / kPhiloxThreads;
+    if (bx < 1) bx = 1;
+    const uint64_t cap = (uint64_t)sms * occ * 4;
+    uint64_t by = nseg < 65535u ? nseg : 65535u;
+    if (bx * by > cap) bx = (cap + by - 1) / by;
+    if (bx < 1) bx = 1;
+    const UniformSpec u = uniform_spec_f32(a, b);
+    if (u.plan == kPlanTwoPass) return fail(PRNG_ERR_INVALID_RANGE, "segment range too narrow for fp32");
+    const XformParams p = u.p;
+    philox_segments_kernel<kUniformF32><<<dim3((unsigned)bx, (unsigned)by), kPhiloxThreads, 0, (cudaStream_t)stream>>>(
+        k0, k1, reinterpret_cast<const PhiloxSegment*>(segs), nseg, p, (float*)dptr);
+    PRNG_CUDA(cudaGetLastError());
+    return PRNG_OK;
+}
+
+int prng_kernels_philox_fill(uint32_t k0, uint32_t k1, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
+                             uint32_t offset, uint64_t n, uint32_t* host_out) {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    if (n == 0) return PRNG_OK;
+    if (!host_out) return fail(PRNG_ERR_INVALID_PARAMETER, "host_out must not be NULL");
+    if (offset > 3) return fail(PRNG_ERR_INVALID_PARAMETER, "offset must be 0..3, got %u", offset);
+    void* d = nullptr;
+    cudaStream_t s = nullptr;
+    const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
+    int rc = scratch(chunk * 4, &d, &s);
+    if (rc) return rc;
+    // position of the first word; each chunk restarts from its own offset
+    // exactly as the reference's chunk kernels do (rngburn.py:70-73).
+    u128 pos = (((u128)b3 << 96) | ((u128)b2 << 64) | ((u128)b1 << 32) | b0) * 4 + offset;
+    for (uint64_t done = 0; done < n; done += chunk) {
+        const uint64_t m = (n - done) < chunk ? (n - done) : chunk;
+        const u128 p = pos + done;
+        const u128 blk = p >> 2;
+        const uint32_t ctr[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)(blk >> 64), (uint32_t)(blk >> 96)};
+        rc = launch_philox<kBits>(k0, k1, ctr, (uint32_t)(p & 3), m, d, XformParams{}, s);
+        if (rc) return rc;
+        PRNG_CUDA(cudaMemcpyAsync(host_out + done, d, m * 4, cudaMemcpyDeviceToHost, s));
+    }
+    PRNG_CUDA(cudaStreamSynchronize(s));
+    return PRNG_OK;
+}
+
+int prng_kernels_mrg_fill(uint32_t s10, uint32_t s11, uint32_t s12, uint32_t s20, uint32_t s21, uint32_t s22,
+                          uint64_t n, uint32_t* host_out, uint32_t s1_out[3], uint32_t s2_out[3]) {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    uint32_t s1[3] = {s10, s11, s12}, s2[3] = {s20, s21, s22};
+    int rc = check_mrg_state(s1, s2);
+    if (rc) return rc;
+    if (n && !host_out) return fail(PRNG_ERR_INVALID_PARAMETER, "host_out must not be NULL");
+    void* d = nullptr;
+    cudaStream_t s = nullptr;
+    const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
+    if (n) {
+        rc = scratch(chunk * 4, &d, &s);
+        if (rc) return rc;
+    }
+    uint32_t c1[3] = {s10, s11, s12}, c2[3] = {s20, s21, s22};
+    for (uint64_t done = 0; done < n; done += chunk) {
+        const uint64_t m = (n - done) < chunk ? (n - done) : chunk;
+        rc = launch_mrg<kBits>(c1, c2, m, d, XformParams{}, s);
+        if (rc) return rc;
+        PRNG_CUDA(cudaMemcpyAsync(host_out + done, d, m * 4, cudaMemcpyDeviceToHost, s));
+        rc = prng_mrg32k3a_skip_ahead(c1, c2, m, 0, c1, c2);
+        if (rc) return rc;
+    }
+    if (n) PRNG_CUDA(cudaStreamSynchronize(s));
+    if (s1_out && s2_out)
+        for (int i = 0; i < 3; ++i) {
+            s1_out[i] = c1[i];
+            s2_out[i] = c2[i];
+        }
+    return PRNG_OK;
+}
+
+int prng_kernels_box_muller(const double* u1, const double* u2, uint64_t m, double* z0, double* z1) {
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    if (m == 0) return PRNG_OK;
+    if (!u1 || !u2 || !z0 || !z1) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL array");
+    void* d = nullptr;
+    cudaStream_t s = nullptr;
+    int rc = scratch(m * 32, &d, &s);
+    if (rc) return rc;
+    double* du1 = (double*)d;
+    double* du2 = du1 + m;
+    double* dz0 = du2 + m;
+    double* dz1 = dz0 + m;
+    PRNG_CUDA(cudaMemcpyAsync(du1, u1, m * 8, cudaMemcpyHostToDevice, s));
+    PRNG_CUDA(cudaMemcpyAsync(du2, u2, m * 8, cudaMemcpyHostToDevice, s));
+    uint64_t blocks = (m + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    box_muller_kernel<<<(unsigned)blocks, 256, 0, s>>>(du1, du2, m, dz0, dz1);
+    PRNG_CUDA(cudaGetLastError());
+    PRNG_CUDA(cudaMemcpyAsync(z0, dz0, m * 8, cudaMemcpyDeviceToHost, s));
+    PRNG_CUDA(cudaMemcpyAsync(z1, dz1, m * 8, cudaMemcpyDeviceToHost, s));
+    PRNG_CUDA(cudaStreamSynchronize(s));
+    return PRNG_OK;
+}
+
+}  // extern "C"

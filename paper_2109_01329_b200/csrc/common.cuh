@@ -1,0 +1,303 @@
+// common.cuh -- shared device code for the B200 RNG kernels.
+//
+// Engine arithmetic (Philox4x32-10, MRG32k3a modular steps) and the fused
+// distribution transforms.  Every transform reproduces the reference's
+// rounding sequence explicitly (no FMA contraction where the reference has
+// two roundings), see the per-function citations.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace prng {
+
+// engine.py:34-37 / _core.pyx:12-15
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+// engine.py:41-46
+constexpr uint32_t kMrgM1 = 4294967087u;  // 2^32 - 209
+constexpr uint32_t kMrgM2 = 4294944443u;  // 2^32 - 22853
+constexpr uint32_t kMrgC1 = 209u;
+constexpr uint32_t kMrgC2 = 22853u;
+constexpr uint32_t kMrgA12 = 1403580u;
+constexpr uint32_t kMrgA13N = 810728u;
+constexpr uint32_t kMrgA21 = 527612u;
+constexpr uint32_t kMrgA23N = 1370589u;
+
+constexpr float kUnitF = 5.9604644775390625e-08f;  // 2^-24 (distributions.py:24)
+constexpr double kUnitD = 5.9604644775390625e-08;
+constexpr double kTwoPi = 6.283185307179586;  // distributions.py:25, _core.pyx:17
+
+struct U4 {
+    uint32_t x, y, z, w;
+};
+
+// One Philox4x32-10 block (engine.py:86-103, _core.pyx:20-39).  The round
+// keys k + i*W are kernel-uniform, so ptxas keeps them in uniform registers;
+// each round is two IMAD.WIDE.U32 and two 3-input LOP3s.
+__device__ __forceinline__ U4 philox_block(uint32_t k0, uint32_t k1, U4 c) {
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+        const uint64_t p0 = (uint64_t)kPhiloxM0 * c.x;
+        const uint64_t p1 = (uint64_t)kPhiloxM1 * c.z;
+        const uint32_t t0 = (uint32_t)(p1 >> 32) ^ c.y ^ k0;
+        const uint32_t t2 = (uint32_t)(p0 >> 32) ^ c.w ^ k1;
+        c.y = (uint32_t)p1;
+        c.w = (uint32_t)p0;
+        c.x = t0;
+        c.z = t2;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+    return c;
+}
+
+// 128-bit counter (lo64, hi64) + idx, carried across all four lanes
+// (_core.pyx:63-70).
+__device__ __forceinline__ U4 counter_add(uint64_t lo, uint64_t hi, uint64_t idx) {
+    const uint64_t l = lo + idx;
+    const uint64_t h = hi + (l < lo ? 1u : 0u);
+    return U4{(uint32_t)l, (uint32_t)(l >> 32), (uint32_t)h, (uint32_t)(h >> 32)};
+}
+
+__device__ __forceinline__ uint32_t lane_of(const U4& b, uint32_t i) {
+    return i == 0 ? b.x : i == 1 ? b.y : i == 2 ? b.z : b.w;
+}
+
+// ---------------------------------------------------------------- MRG32k3a
+// x mod m for m = 2^32 - c, x < 2^64 (two folds of 2^32 == c, one subtract).
+template <uint32_t C>
+__device__ __forceinline__ uint32_t fold_mod(uint64_t t) {
+    constexpr uint64_t M = (1ull << 32) - C;
+    t = (t >> 32) * C + (t & 0xffffffffull);
+    t = (t >> 32) * C + (t & 0xffffffffull);
+    return (uint32_t)(t >= M ? t - M : t);
+}
+
+// One MRG32k3a step of both components (_core.pyx:85-101).  Signed products
+// are offset by a multiple of the modulus to stay in unsigned 64-bit:
+// a12*x11 - a13n*x10 + 2^20*m1 is in [0, 2^53.3); a21*x22 - a23n*x20 + 2^21*m2
+// in [0, 2^53.4).  Returns z = (p1 - p2) mod m1.
+struct MrgState {
+    uint32_t x10, x11, x12, x20, x21, x22;
+};
+
+__device__ __forceinline__ uint32_t mrg_step(MrgState& s) {
+    const uint64_t t1 = (uint64_t)kMrgA12 * s.x11 + (((uint64_t)kMrgM1 << 20) - (uint64_t)kMrgA13N * s.x10);
+    const uint64_t t2 = (uint64_t)kMrgA21 * s.x22 + (((uint64_t)kMrgM2 << 21) - (uint64_t)kMrgA23N * s.x20);
+    const uint32_t p1 = fold_mod<kMrgC1>(t1);
+    const uint32_t p2 = fold_mod<kMrgC2>(t2);
+    s.x10 = s.x11; s.x11 = s.x12; s.x12 = p1;
+    s.x20 = s.x21; s.x21 = s.x22; s.x22 = p2;
+    return p1 >= p2 ? p1 - p2 : p1 - p2 + kMrgM1;
+}
+
+// y = J x mod m (3x3), products folded before summation.
+template <uint32_t C>
+__device__ __forceinline__ void mat3_apply(const uint32_t* J, uint32_t& a, uint32_t& b, uint32_t& c) {
+    uint32_t r[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const uint64_t s = (uint64_t)fold_mod<C>((uint64_t)J[3 * i] * a) +
+                           (uint64_t)fold_mod<C>((uint64_t)J[3 * i + 1] * b) +
+                           (uint64_t)fold_mod<C>((uint64_t)J[3 * i + 2] * c);
+        r[i] = fold_mod<C>(s);
+    }
+    a = r[0]; b = r[1]; c = r[2];
+}
+
+// ---------------------------------------------------------- transforms
+// Word -> unit: (w >> 8) * 2^-24, exact in fp32 and fp64 (distributions.py:78-87).
+__device__ __forceinline__ float unit_f32(uint32_t w) { return __fmul_rn((float)(w >> 8), kUnitF); }
+__device__ __forceinline__ double unit_f64(uint32_t w) { return __dmul_rn((double)(w >> 8), kUnitD); }
+
+// Parameters of one fused request.  For uniform: (a, b) -> scale/offset with
+// the reference's precision rules (distributions.py:98-104 under numpy
+// NEP-50: fp32 arrays see f32(hi - lo) and f32(lo)).
+struct XformParams {
+    float scale_f, off_f;    // uniform fp32: f32(b - a) * 2^-24, f32(a); gaussian fp32: stddev, mean
+    double scale_d, off_d;   // uniform fp64: (b - a) * 2^-24, a; gaussian fp64: stddev, mean
+    double ln_scale, ln_displ;  // lognormal: scale, displ (fp64 path) ...
+    float ln_scale_f, ln_displ_f;  // ... and fp32 path
+};
+
+// Transform kinds (template parameter).
+enum Xform : int {
+    kBits = 0,
+    kUniformF32 = 1,
+    kUniformF64 = 2,
+    kGaussF32Fast = 3,
+    kGaussF32Accurate = 4,
+    kGaussF64 = 5,
+    kLognF32Fast = 6,
+    kLognF32Accurate = 7,
+    kLognF64 = 8,
+    kUnitF32 = 9,   // uniform on [0, 1): the affine pass is an exact identity
+    kUnitF64 = 10,
+};
+
+template <int X> struct XformTraits;
+template <> struct XformTraits<kBits> { using T = uint32_t; static constexpr bool kPair = false; };
+template <> struct XformTraits<kUniformF32> { using T = float; static constexpr bool kPair = false; };
+template <> struct XformTraits<kUniformF64> { using T = double; static constexpr bool kPair = false; };
+template <> struct XformTraits<kUnitF32> { using T = float; static constexpr bool kPair = false; };
+template <> struct XformTraits<kUnitF64> { using T = double; static constexpr bool kPair = false; };
+template <> struct XformTraits<kGaussF32Fast> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kGaussF32Accurate> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kGaussF64> { using T = double; static constexpr bool kPair = true; };
+template <> struct XformTraits<kLognF32Fast> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kLognF32Accurate> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kLognF64> { using T = double; static constexpr bool kPair = true; };
+
+// Single-word transforms.
+template <int X>
+__device__ __forceinline__ typename XformTraits<X>::T xform1(uint32_t w, const XformParams& p);
+
+template <> __device__ __forceinline__ uint32_t xform1<kBits>(uint32_t w, const XformParams&) { return w; }
+
+template <> __device__ __forceinline__ float xform1<kUnitF32>(uint32_t w, const XformParams&) { return unit_f32(w); }
+template <> __device__ __forceinline__ double xform1<kUnitF64>(uint32_t w, const XformParams&) { return unit_f64(w); }
+
+// fl(fl(u * S) + off) with u = (w >> 8) * 2^-24.  Because the 2^-24 factor is
+// a power of two, fl(u * S) == fl((w >> 8) * S') with S' = S * 2^-24 (exact;
+// the host only takes this path when S' is a normal number), which saves one
+// multiply per sample.  The add is a separate rounding: never an FMA.
+template <> __device__ __forceinline__ float xform1<kUniformF32>(uint32_t w, const XformParams& p) {
+    return __fadd_rn(__fmul_rn((float)(w >> 8), p.scale_f), p.off_f);
+}
+
+template <> __device__ __forceinline__ double xform1<kUniformF64>(uint32_t w, const XformParams& p) {
+    return __dadd_rn(__dmul_rn((double)(w >> 8), p.scale_d), p.off_d);
+}
+
+// Box-Muller on one word pair (distributions.py:107-131, _core.pyx:116-121):
+// u1' = 1 - u1 in (0, 1], r = sqrt(-2 ln u1'), t = 2 pi u2, (r cos t, r sin t).
+//
+// Accurate (fp64) route: the reference's own formula in double precision with
+// CUDA's libdevice log / sincos (<= 1 / 2 ulp), then `z*stddev + mean` as two
+// roundings (distributions.py:129-130).
+__device__ __forceinline__ void box_muller_f64(uint32_t w0, uint32_t w1, double& z0, double& z1) {
+    const double u1 = 1.0 - unit_f64(w0);
+    const double u2 = unit_f64(w1);
+    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+    const double t = __dmul_rn(kTwoPi, u2);
+    double s, c;
+    sincos(t, &s, &c);
+    z0 = __dmul_rn(r, c);
+    z1 = __dmul_rn(r, s);
+}
+
+// Fast (fp32) route: u1' = (2^24 - (w0 >> 8)) * 2^-24 is exact; logf is
+// accurate to 1 ulp including near 1; 2*u2 is exact so sincospif evaluates
+// cos/sin(2 pi u2) without the fp32 rounding of 2 pi * u2.
+__device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {
+    const float u1 = __fmul_rn((float)(16777216u - (w0 >> 8)), kUnitF);
+    const float x2 = __fmul_rn((float)(w1 >> 8), 1.1920928955078125e-07f);  // 2 * u2, exact
+    const float r = sqrtf(-2.0f * logf(u1));
+    float s, c;
+    sincospif(x2, &s, &c);
+    z0 = r * c;
+    z1 = r * s;
+}
+
+template <int X>
+__device__ __forceinline__ void xform2(uint32_t w0, uint32_t w1, const XformParams& p,
+                                       typename XformTraits<X>::T& o0, typename XformTraits<X>::T& o1);
+
+template <> __device__ __forceinline__ void xform2<kGaussF64>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                             double& o0, double& o1) {
+    double z0, z1;
+    box_muller_f64(w0, w1, z0, z1);
+    o0 = __dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);
+    o1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
+}
+
+template <> __device__ __forceinline__ void xform2<kGaussF32Accurate>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                     float& o0, float& o1) {
+    double z0, z1;
+    box_muller_f64(w0, w1, z0, z1);
+    o0 = (float)__dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);
+    o1 = (float)__dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
+}
+
+template <> __device__ __forceinline__ void xform2<kGaussF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                 float& o0, float& o1) {
+    float z0, z1;
+    box_muller_f32(w0, w1, z0, z1);
+    o0 = fmaf(z0, p.scale_f, p.off_f);
+    o1 = fmaf(z1, p.scale_f, p.off_f);
+}
+
+// Lognormal (extension a18): x = exp(m + s*z) * scale + displ.
+template <> __device__ __forceinline__ void xform2<kLognF64>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                            double& o0, double& o1) {
+    double z0, z1;
+    box_muller_f64(w0, w1, z0, z1);
+    const double g0 = __dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);
+    const double g1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
+    o0 = __dadd_rn(__dmul_rn(exp(g0), p.ln_scale), p.ln_displ);
+    o1 = __dadd_rn(__dmul_rn(exp(g1), p.ln_scale), p.ln_displ);
+}
+
+template <> __device__ __forceinline__ void xform2<kLognF32Accurate>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                    float& o0, float& o1) {
+    double a, b;
+    xform2<kLognF64>(w0, w1, p, a, b);
+    o0 = (float)a;
+    o1 = (float)b;
+}
+
+template <> __device__ __forceinline__ void xform2<kLognF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                float& o0, float& o1) {
+    float z0, z1;
+    box_muller_f32(w0, w1, z0, z1);
+    o0 = fmaf(expf(fmaf(z0, p.scale_f, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+    o1 = fmaf(expf(fmaf(z1, p.scale_f, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+}
+
+// Four consecutive stream words -> four outputs.  For pair transforms the
+// group must start on a pair boundary (relative to the request start).
+template <int X>
+__device__ __forceinline__ void xform4(const U4& w, const XformParams& p, typename XformTraits<X>::T o[4]) {
+    if constexpr (XformTraits<X>::kPair) {
+        xform2<X>(w.x, w.y, p, o[0], o[1]);
+        xform2<X>(w.z, w.w, p, o[2], o[3]);
+    } else {
+        o[0] = xform1<X>(w.x, p);
+        o[1] = xform1<X>(w.y, p);
+        o[2] = xform1<X>(w.z, p);
+        o[3] = xform1<X>(w.w, p);
+    }
+}
+
+// ---------------------------------------------------------------- stores
+// Streaming (evict-first) vector stores: every sample is written once and
+// never re-read by the kernel.
+__device__ __forceinline__ void st_group(uint32_t* p, const uint32_t o[4]) {
+    asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_group(float* p, const float o[4]) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(o[0]), "f"(o[1]), "f"(o[2]), "f"(o[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_group(double* p, const double o[4]) {
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(o[0]), "d"(o[1]), "d"(o[2]), "d"(o[3])
+                 : "memory");
+}
+// Two adjacent 4-byte groups as one 256-bit store.
+__device__ __forceinline__ void st_group2(uint32_t* p, const uint32_t a[4], const uint32_t b[4]) {
+    asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(a[0]), "r"(a[1]), "r"(a[2]),
+                 "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_group2(float* p, const float a[4], const float b[4]) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a[0]), "f"(a[1]), "f"(a[2]),
+                 "f"(a[3]), "f"(b[0]), "f"(b[1]), "f"(b[2]), "f"(b[3])
+                 : "memory");
+}
+
+}  // namespace prng

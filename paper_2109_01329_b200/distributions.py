@@ -1,0 +1,264 @@
+"""Distribution requests and the fused device generators.
+
+Mirrors pkg/src/portarng/distributions.py (names, validation, word
+accounting, precision rules) and adds the oneMKL-style entry point
+``generate(distribution, engine_state, n, out)`` the north star names, plus
+``UniformBits`` and ``Lognormal``.
+
+Every generator is ONE kernel launch (libprng_b200.so) that draws the words,
+applies the distribution transform and writes each sample to HBM once; the
+reference's separate generate -> words_to_unit -> range_transform passes
+(rngburn.py:142-147) are fused.  Outputs live on the GPU as torch tensors.
+
+Results vs the reference:
+  * uniform_bits, uniform fp32/fp64 on [a, b): bit-exact;
+  * gaussian/lognormal fp64, and fp32 with method="accurate": fp64 math on
+    the device (CUDA libdevice log/sincos/exp vs glibc), a few fp64 ulps;
+  * gaussian/lognormal fp32 with method="fast" (default): fp32 logf /
+    sqrtf / sincospif / expf, within the stated fp32 tolerance.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+from typing import Tuple, Union
+
+from . import _lib
+from .engine import (
+    EngineState,
+    Mrg32k3aState,
+    PhiloxState,
+    _out_tensor,
+    _stream_handle,
+    _torch,
+    advance,
+    generate_words,
+    mrg_args,
+    philox_args,
+)
+from .errors import InvalidParameter, InvalidRange, UnsupportedEngine
+
+_UNIT_SCALE = 2.0 ** -24
+_PRECISIONS = ("fp32", "fp64")
+_METHODS = {"fast": _lib.METHOD_FAST, "accurate": _lib.METHOD_ACCURATE}
+
+
+def _check_precision(precision: str) -> None:
+    if precision not in _PRECISIONS:
+        raise InvalidParameter(f"precision must be fp32 or fp64, got {precision!r}")
+
+
+def _check_method(method: str) -> None:
+    if method not in _METHODS:
+        raise InvalidParameter(f"method must be 'fast' or 'accurate', got {method!r}")
+
+
+def _dtype(precision: str):
+    torch = _torch()
+    return torch.float32 if precision == "fp32" else torch.float64
+
+
+@dataclass(frozen=True)
+class Uniform:
+    """Uniform draw request over [lo, hi) (distributions.py:38-49)."""
+
+    lo: float
+    hi: float
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if not (math.isfinite(self.lo) and math.isfinite(self.hi)) or self.lo >= self.hi:
+            raise InvalidRange(f"uniform range requires finite lo < hi, got [{self.lo}, {self.hi})")
+        _check_precision(self.precision)
+
+
+@dataclass(frozen=True)
+class Gaussian:
+    """Normal draw request (distributions.py:52-63); Box-Muller pairs."""
+
+    mean: float
+    stddev: float
+    precision: str = "fp32"
+    method: str = "fast"
+
+    def __post_init__(self):
+        if not math.isfinite(self.mean) or not math.isfinite(self.stddev) or self.stddev <= 0:
+            raise InvalidParameter(f"gaussian requires finite mean and stddev > 0, got ({self.mean}, {self.stddev})")
+        _check_precision(self.precision)
+        _check_method(self.method)
+
+
+@dataclass(frozen=True)
+class Lognormal:
+    """Lognormal request x = displ + scale * exp(m + s z) (oneMKL lognormal;
+    absent from the reference)."""
+
+    m: float = 0.0
+    s: float = 1.0
+    displ: float = 0.0
+    scale: float = 1.0
+    precision: str = "fp32"
+    method: str = "fast"
+
+    def __post_init__(self):
+        vals = (self.m, self.s, self.displ, self.scale)
+        if not all(math.isfinite(v) for v in vals) or self.s <= 0 or self.scale <= 0:
+            raise InvalidParameter(f"lognormal requires finite m, s > 0, finite displ, scale > 0, got {vals}")
+        _check_precision(self.precision)
+        _check_method(self.method)
+
+
+@dataclass(frozen=True)
+class UniformBits:
+    """Raw 32-bit words (oneMKL uniform_bits<uint32>)."""
+
+
+DistributionSpec = Union[Uniform, Gaussian, Lognormal, UniformBits]
+
+
+@dataclass
+class RandomBlock:
+    """A generated batch (distributions.py:69-75); `values` is a CUDA tensor."""
+
+    values: object
+    count: int
+    precision: str = "fp32"
+
+
+def words_consumed(spec: DistributionSpec, n: int) -> int:
+    """Stream words a request of n samples consumes (distributions.py:146-149)."""
+    if isinstance(spec, (Gaussian, Lognormal)):
+        return 2 * ((n + 1) // 2)
+    return n
+
+
+def word_to_unit(w: int) -> float:
+    """distributions.py:78-80 (scalar helper; exact arithmetic)."""
+    return (w >> 8) * _UNIT_SCALE
+
+
+def words_to_unit(words, precision: str = "fp32", out=None, stream=None):
+    """Device words -> unit values, (w >> 8) * 2**-24 (distributions.py:83-87)."""
+    _check_precision(precision)
+    n = words.numel()
+    out = _out_tensor(out, n, _dtype(precision), words.device)
+    fn = _lib.lib.prng_words_to_unit_f32 if precision == "fp32" else _lib.lib.prng_words_to_unit_f64
+    _lib.check(fn(words.data_ptr(), n, out.data_ptr(), _stream_handle(stream, out.device)))
+    return out[:n]
+
+
+def gaussian_from_words(words, mean: float, stddev: float, n: int, precision: str = "fp32",
+                        method: str = "fast", out=None, stream=None):
+    """distributions.py:116-131 on device words (2*ceil(n/2) of them)."""
+    _check_precision(precision)
+    _check_method(method)
+    if words.numel() < 2 * ((n + 1) // 2):
+        raise InvalidParameter("need 2*ceil(n/2) words")
+    out = _out_tensor(out, n, _dtype(precision), words.device)
+    s = _stream_handle(stream, out.device)
+    if precision == "fp32":
+        rc = _lib.lib.prng_gaussian_from_words_f32(words.data_ptr(), n, mean, stddev, _METHODS[method],
+                                                   out.data_ptr(), s)
+    else:
+        rc = _lib.lib.prng_gaussian_from_words_f64(words.data_ptr(), n, mean, stddev, out.data_ptr(), s)
+    _lib.check(rc)
+    return out[:n]
+
+
+def _launch(spec: DistributionSpec, state: EngineState, n: int, ptr: int, s) -> None:
+    L = _lib.lib
+    if isinstance(state, PhiloxState):
+        k0, k1, ctr, lane = philox_args(state)
+        head = (k0, k1, ctr, lane, n)
+        prefix = "prng_philox4x32x10_"
+    elif isinstance(state, Mrg32k3aState):
+        s1, s2 = mrg_args(state)
+        head = (s1, s2, n)
+        prefix = "prng_mrg32k3a_"
+    else:
+        raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+    if isinstance(spec, UniformBits):
+        rc = getattr(L, prefix + "bits")(*head, ptr, s)
+    elif isinstance(spec, Uniform):
+        rc = getattr(L, prefix + "uniform_" + ("f32" if spec.precision == "fp32" else "f64"))(
+            *head, spec.lo, spec.hi, ptr, s)
+    elif isinstance(spec, Gaussian):
+        if spec.precision == "fp32":
+            rc = getattr(L, prefix + "gaussian_f32")(*head, spec.mean, spec.stddev, _METHODS[spec.method], ptr, s)
+        else:
+            rc = getattr(L, prefix + "gaussian_f64")(*head, spec.mean, spec.stddev, ptr, s)
+    elif isinstance(spec, Lognormal):
+        if spec.precision == "fp32":
+            rc = getattr(L, prefix + "lognormal_f32")(*head, spec.m, spec.s, spec.displ, spec.scale,
+                                                       _METHODS[spec.method], ptr, s)
+        else:
+            rc = getattr(L, prefix + "lognormal_f64")(*head, spec.m, spec.s, spec.displ, spec.scale, ptr, s)
+    else:
+        raise InvalidParameter(f"unknown distribution {spec!r}")
+    _lib.check(rc)
+
+
+def out_dtype(spec: DistributionSpec):
+    torch = _torch()
+    if isinstance(spec, UniformBits):
+        return torch.uint32
+    return _dtype(spec.precision)
+
+
+def generate(distribution: DistributionSpec, engine: EngineState, n: int, out=None, stream=None):
+    """oneMKL-style generate(distr, engine, n, r): n samples into `out`
+    (a CUDA tensor; allocated if None) on `stream`.  Returns
+    (advanced_engine_state, out[:n]).  One fused kernel launch."""
+    if n < 0:
+        raise InvalidParameter("count must be non-negative")
+    out = _out_tensor(out, n, out_dtype(distribution))
+    if n:
+        _launch(distribution, engine, n, out.data_ptr(), _stream_handle(stream, out.device))
+    new_state = advance(engine, words_consumed(distribution, n))
+    return new_state, (out if out.numel() == n else out[:n])
+
+
+def fill_uniform_unit(state: EngineState, n: int, precision: str = "fp32", out=None, stream=None):
+    """distributions.py:90-95: n unit uniforms; state advances n words."""
+    if n < 0:
+        raise InvalidParameter("count must be non-negative")
+    _check_precision(precision)
+    state, values = generate(Uniform(0.0, 1.0, precision), state, n, out, stream)
+    return state, RandomBlock(values=values, count=n, precision=precision)
+
+
+def fill_uniform(state: EngineState, n: int, lo: float, hi: float, precision: str = "fp32", out=None,
+                 stream=None):
+    """Fused fill_uniform_unit + range_transform (one pass, bit-identical)."""
+    state, values = generate(Uniform(lo, hi, precision), state, n, out, stream)
+    return state, RandomBlock(values=values, count=n, precision=precision)
+
+
+def range_transform(block: RandomBlock, lo: float, hi: float, stream=None) -> RandomBlock:
+    """distributions.py:98-104: in-place affine map of unit values onto [lo, hi)."""
+    if not (math.isfinite(lo) and math.isfinite(hi)) or lo >= hi:
+        raise InvalidRange(f"range transform requires finite lo < hi, got [{lo}, {hi})")
+    v = block.values
+    fn = _lib.lib.prng_range_transform_f32 if block.precision == "fp32" else _lib.lib.prng_range_transform_f64
+    _lib.check(fn(v.data_ptr(), v.numel(), lo, hi, _stream_handle(stream, v.device)))
+    return block
+
+
+def fill_gaussian(state: EngineState, n: int, mean: float, stddev: float, precision: str = "fp32",
+                  out=None, stream=None, method: str = "fast"):
+    """distributions.py:134-153: n normals, state advances 2*ceil(n/2) words."""
+    if n < 0:
+        raise InvalidParameter("count must be non-negative")
+    state, values = generate(Gaussian(mean, stddev, precision, method), state, n, out, stream)
+    return state, RandomBlock(values=values, count=n, precision=precision)
+
+
+def fill_lognormal(state: EngineState, n: int, m: float = 0.0, s: float = 1.0, displ: float = 0.0,
+                   scale: float = 1.0, precision: str = "fp32", out=None, stream=None, method: str = "fast"):
+    """Lognormal extension; state advances 2*ceil(n/2) words."""
+    if n < 0:
+        raise InvalidParameter("count must be non-negative")
+    state, values = generate(Lognormal(m, s, displ, scale, precision, method), state, n, out, stream)
+    return state, RandomBlock(values=values, count=n, precision=precision)

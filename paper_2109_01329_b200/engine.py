@@ -1,0 +1,239 @@
+"""Engine states and stream-position bookkeeping (host side of the hot path).
+
+Mirrors pkg/src/portarng/engine.py: same names, state types, seed mapping
+and error behaviour.  What changes:
+
+* every word is produced on the GPU (libprng_b200.so) -- `generate_words`
+  returns a device tensor, and even the scalar `philox_block` / `next_word`
+  helpers run on the device: there is no CPU compute path;
+* `skip_ahead` also works for MRG32k3a (matrix-power jump-ahead, computed
+  by the C library's host code; the reference raises UnsupportedEngine,
+  engine.py:201-202).
+
+The state bookkeeping itself (128-bit positions, lanes, windows) is plain
+integer arithmetic on the host, exactly as in the reference
+(engine.py:125-146, 194-209).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+from dataclasses import dataclass
+from typing import Optional, Tuple, Union
+
+from . import _lib
+from .errors import InvalidParameter, UnsupportedEngine
+
+MASK32 = 0xFFFFFFFF
+MASK64 = 0xFFFFFFFFFFFFFFFF
+MASK128 = (1 << 128) - 1
+
+PHILOX_M0 = 0xD2511F53
+PHILOX_M1 = 0xCD9E8D57
+PHILOX_W0 = 0x9E3779B9
+PHILOX_W1 = 0xBB67AE85
+PHILOX_ROUNDS = 10
+
+MRG_M1 = 4294967087
+MRG_M2 = 4294944443
+MRG_A12 = 1403580
+MRG_A13N = 810728
+MRG_A21 = 527612
+MRG_A23N = 1370589
+MRG_DEFAULT_SEED = 12345
+
+
+class EngineKind(enum.Enum):
+    PHILOX4X32X10 = "philox"
+    MRG32K3A = "mrg32k3a"
+
+
+@dataclass(frozen=True)
+class PhiloxState:
+    """Philox stream position (engine.py:57-72): key pair, 128-bit counter of
+    the next block, lane_index in 0..4 (4 = no block buffered)."""
+
+    key: Tuple[int, int]
+    counter: Tuple[int, int, int, int]
+    lane_index: int
+    cached_block: Optional[Tuple[int, int, int, int]] = None
+
+
+@dataclass(frozen=True)
+class Mrg32k3aState:
+    """MRG32k3a recurrence windows (engine.py:75-80)."""
+
+    s1: Tuple[int, int, int]
+    s2: Tuple[int, int, int]
+
+
+EngineState = Union[PhiloxState, Mrg32k3aState]
+
+
+def seed_engine(kind: EngineKind, seed: int) -> EngineState:
+    """engine.py:106-122: Philox key = (seed lo32, hi32), counter 0, lane 4;
+    MRG32k3a all six components = seed mod m2 (0 -> 12345)."""
+    seed &= MASK64
+    if kind is EngineKind.PHILOX4X32X10:
+        return PhiloxState(key=(seed & MASK32, seed >> 32), counter=(0, 0, 0, 0), lane_index=4)
+    if kind is EngineKind.MRG32K3A:
+        v = seed % MRG_M2
+        if v == 0:
+            v = MRG_DEFAULT_SEED
+        return Mrg32k3aState(s1=(v, v, v), s2=(v, v, v))
+    raise UnsupportedEngine(f"unknown engine kind: {kind!r}")
+
+
+def _ctr_to_int(counter) -> int:
+    return counter[0] | counter[1] << 32 | counter[2] << 64 | counter[3] << 96
+
+
+def _int_to_ctr(value: int) -> Tuple[int, int, int, int]:
+    value &= MASK128
+    return (value & MASK32, (value >> 32) & MASK32, (value >> 64) & MASK32, (value >> 96) & MASK32)
+
+
+def _position(state: PhiloxState) -> int:
+    c = _ctr_to_int(state.counter)
+    if state.lane_index == 4:
+        return 4 * c
+    return 4 * ((c - 1) % (1 << 128)) + state.lane_index
+
+
+def _state_at(key, position: int) -> PhiloxState:
+    block, lane = divmod(position, 4)
+    if lane == 0:
+        return PhiloxState(key=key, counter=_int_to_ctr(block), lane_index=4)
+    return PhiloxState(key=key, counter=_int_to_ctr(block + 1), lane_index=lane)
+
+
+def stream_position(state: PhiloxState) -> int:
+    """engine.py:183-191 (Philox only)."""
+    if not isinstance(state, PhiloxState):
+        raise UnsupportedEngine("stream positions are defined for Philox states")
+    return _position(state)
+
+
+def philox_args(state: PhiloxState):
+    """(k0, k1, ctr[4], lane) of the next word -- the C-ABI Philox state
+    arguments (philox_fill's (k0, k1, b0..b3, offset), engine.py:221-225)."""
+    block, lane = divmod(_position(state), 4)
+    return state.key[0] & MASK32, state.key[1] & MASK32, _lib.u32_array(_int_to_ctr(block)), lane
+
+
+def mrg_args(state: Mrg32k3aState):
+    return _lib.u32_array(state.s1), _lib.u32_array(state.s2)
+
+
+def _mrg_skip(state: Mrg32k3aState, n: int) -> Mrg32k3aState:
+    s1, s2 = mrg_args(state)
+    o1 = (ctypes.c_uint32 * 3)()
+    o2 = (ctypes.c_uint32 * 3)()
+    _lib.check(_lib.lib.prng_mrg32k3a_skip_ahead(s1, s2, n & MASK64, (n >> 64) & MASK64, o1, o2))
+    return Mrg32k3aState(tuple(o1), tuple(o2))
+
+
+def skip_ahead(state: EngineState, n: int) -> EngineState:
+    """Advance by n words as if drawn and discarded (engine.py:194-209).
+
+    Philox: O(1) counter arithmetic.  MRG32k3a: A^n s mod m (extension; the
+    reference raises UnsupportedEngine here).  n < 0 raises ValueError; n == 0
+    returns the same object.
+    """
+    if not isinstance(state, (PhiloxState, Mrg32k3aState)):
+        raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+    if n < 0:
+        raise ValueError("skip count must be non-negative")
+    if n == 0:
+        return state
+    if isinstance(state, Mrg32k3aState):
+        return _mrg_skip(state, n)
+    return _state_at(state.key, _position(state) + n)
+
+
+def advance(state: EngineState, nwords: int) -> EngineState:
+    """State after a request that consumed `nwords` words (no identity shortcut)."""
+    return skip_ahead(state, nwords) if nwords else state
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_handle(stream, device=None):
+    if stream is None:
+        torch = _torch()
+        if device is not None and torch.device(device).type != "cuda":
+            device = None
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _out_tensor(out, n, dtype, device=None):
+    torch = _torch()
+    if out is None:
+        return torch.empty(n, dtype=dtype, device=device if device is not None else "cuda")
+    if out.dtype != dtype:
+        raise InvalidParameter(f"out has dtype {out.dtype}, expected {dtype}")
+    if not out.is_cuda and not out.is_pinned():
+        raise InvalidParameter("out must be a CUDA tensor or pinned host memory")
+    if not out.is_contiguous() or out.numel() < n:
+        raise InvalidParameter(f"out must be contiguous with at least {n} elements")
+    return out
+
+
+def generate_words(state: EngineState, n: int, out=None, stream=None):
+    """n raw 32-bit words on the device; equivalent to n `next_word` calls
+    (engine.py:212-232).  Returns (new_state, uint32 CUDA tensor)."""
+    if n < 0:
+        raise ValueError("word count must be non-negative")
+    if not isinstance(state, (PhiloxState, Mrg32k3aState)):
+        raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+    torch = _torch()
+    out = _out_tensor(out, n, torch.uint32)
+    if n:
+        s = _stream_handle(stream, out.device)
+        if isinstance(state, PhiloxState):
+            k0, k1, ctr, lane = philox_args(state)
+            _lib.check(_lib.lib.prng_philox4x32x10_bits(k0, k1, ctr, lane, n, out.data_ptr(), s))
+        else:
+            s1, s2 = mrg_args(state)
+            _lib.check(_lib.lib.prng_mrg32k3a_bits(s1, s2, n, out.data_ptr(), s))
+    if n == 0:
+        return state, out[:0]
+    return advance(state, n), out[:n] if out.numel() != n else out
+
+
+def philox_block(key: Tuple[int, int], counter: Tuple[int, int, int, int]) -> Tuple[int, int, int, int]:
+    """One Philox4x32-10 block (engine.py:86-103), computed on the device."""
+    state = PhiloxState(key=(key[0] & MASK32, key[1] & MASK32), counter=tuple(counter), lane_index=4)
+    _, words = generate_words(state, 4)
+    return tuple(int(x) for x in words.cpu().tolist())
+
+
+def next_word(state: EngineState):
+    """Draw one word (engine.py:149-175); behavioural helper, device-computed."""
+    if isinstance(state, PhiloxState):
+        if state.lane_index == 4:
+            block = philox_block(state.key, state.counter)
+            ctr = _int_to_ctr(_ctr_to_int(state.counter) + 1)
+            return PhiloxState(state.key, ctr, 1, block), block[0]
+        block = state.cached_block
+        if block is None:
+            block = philox_block(state.key, _int_to_ctr(_ctr_to_int(state.counter) - 1))
+        word = block[state.lane_index]
+        return PhiloxState(state.key, state.counter, state.lane_index + 1, block), word
+    if isinstance(state, Mrg32k3aState):
+        new, words = generate_words(state, 1)
+        return new, int(words.cpu()[0])
+    raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+
+
+def mrg_unit(z: int) -> float:
+    """engine.py:178-180."""
+    return z / (MRG_M1 + 1)

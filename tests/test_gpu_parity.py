@@ -1,0 +1,372 @@
+"""CUDA path vs the oracle and the reference's golden vectors (needs a B200).
+
+Every call goes through the package API -> C ABI (libprng_b200.so) -> the
+sm_100a kernels.  Integer words and uniform fp32/fp64 must be bit-exact;
+gaussian/lognormal must fall within tests/tolerances.py.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2109_01329_b200 as P  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from refcases import case_state, oracle_case  # noqa: E402
+from tolerances import check_close, gaussian_allowed, lognormal_allowed  # noqa: E402
+
+PHILOX = P.EngineKind.PHILOX4X32X10
+MRG = P.EngineKind.MRG32K3A
+
+
+def state_for(engine, seed, skip=0):
+    st = P.seed_engine(PHILOX if engine == "philox" else MRG, seed)
+    return P.skip_ahead(st, skip) if skip else st
+
+
+def spec_for(dist, prec, p0, p1, method="fast"):
+    if dist == "bits":
+        return P.UniformBits()
+    if dist == "uniform":
+        return P.Uniform(p0, p1, prec)
+    if dist == "gaussian":
+        return P.Gaussian(p0, p1, prec, method)
+    return P.Lognormal(p0, p1, 0.0, 1.0, prec, method)
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def compare(dist, prec, got, want, p0, p1, method, name):
+    assert got.dtype == want.dtype, name
+    if dist in ("bits", "uniform"):
+        assert np.array_equal(got, want), name
+        return
+    dt = np.float32 if prec == "fp32" else np.float64
+    fast = method == "fast"
+    if dist == "gaussian":
+        allowed = gaussian_allowed(want, p0, p1, dt, fast)
+    else:
+        allowed = lognormal_allowed(want, p0, p1, dt, fast)
+    check_close(got, want, allowed, name)
+
+
+# --------------------------------------------------------------- golden
+
+
+def test_philox_kat_on_device(golden):
+    for key, ctr, expected in golden["philox_kat"]:
+        assert P.philox_block(tuple(key), tuple(ctr)) == tuple(expected)
+
+
+def test_c1_hashes_2p24(golden):
+    st = P.seed_engine(PHILOX, 777)
+    _, w = P.generate(P.UniformBits(), st, 1 << 24)
+    w = host(w)
+    assert w[:8].tolist() == golden["philox777_words8"]
+    assert O.sha16(w) == golden["philox777_u32_2p24_sha16"]
+    _, u = P.generate(P.Uniform(0.0, 1.0), st, 1 << 24)
+    u = host(u)
+    assert O.sha16(u) == golden["philox777_uniform_f32_2p24_sha16"]
+    assert u[:4].tolist() == golden["philox777_uniform_f32_first4"]
+
+
+def test_other_golden_hashes(golden):
+    st = P.seed_engine(PHILOX, 777)
+    assert O.sha16(host(P.generate(P.Uniform(-1.0, 1.0, "fp64"), st, 1 << 20)[1])) == \
+        golden["philox777_uniform_f64_m1p1_2p20_sha16"]
+    z = host(P.generate(P.Gaussian(0.0, 1.0, "fp32", "accurate"), st, 1 << 20)[1])
+    want = O.generate("philox", (O.seed_philox(777), 0), "gaussian", 1 << 20, "fp32", 0.0, 1.0)
+    # accurate fp32 gaussian: fp64 math then cast -> (almost always) bit-exact
+    _, exact = check_close(z, want, gaussian_allowed(want, 0.0, 1.0, np.float32, False), "gauss acc")
+    assert exact > 0.9999
+    m = P.seed_engine(MRG, 777)
+    mw = host(P.generate(P.UniformBits(), m, 1 << 20)[1])
+    assert mw[:4].tolist() == golden["mrg777_words4"]
+    assert int(mw[-1]) == golden["mrg777_word_2p20m1"]
+    assert O.sha16(mw) == golden["mrg777_u32_2p20_sha16"]
+    mu = host(P.generate(P.Uniform(-1.0, 1.0, "fp64"), m, 1 << 20)[1])
+    assert O.sha16(mu) == golden["mrg777_uniform_f64_m1p1_2p20_sha16"]
+
+
+def test_far_offset(golden):
+    st = P.skip_ahead(P.seed_engine(PHILOX, 777), (1 << 98) + 3)
+    assert host(P.generate_words(st, 16)[1]).tolist() == golden["philox777_far_2p98p3_words16"]
+
+
+def test_all_golden_cases(golden, golden_arrays):
+    for case in golden["cases"]:
+        name, engine, seed, skip, dist, prec, p0, p1, n = case
+        want = golden_arrays[f"case__{name}"]
+        for method in (("fast", "accurate") if dist in ("gaussian", "lognormal") else ("fast",)):
+            st = state_for(engine, seed, skip)
+            new, got = P.generate(spec_for(dist, prec, p0, p1, method), st, n)
+            compare(dist, prec, host(got), want, p0, p1, method, f"{name}/{method}")
+            # state accounting identical to the reference's word consumption
+            used = n if dist in ("bits", "uniform") else 2 * ((n + 1) // 2)
+            assert new == P.skip_ahead(st, used) or (used == 0 and new == st)
+
+
+def test_burn_once_outputs(golden_arrays):
+    _, u = P.generate(P.Uniform(-1.0, 1.0), P.seed_engine(PHILOX, 99), 1000)
+    assert np.array_equal(host(u), golden_arrays["burn__philox_uniform_m1p1_1000"])
+    _, u = P.generate(P.Uniform(-1.0, 1.0), P.seed_engine(MRG, 99), 500)
+    assert np.array_equal(host(u), golden_arrays["burn__mrg_uniform_m1p1_500"])
+    _, u = P.generate(P.Uniform(-1.0, 1.0, "fp64"), P.seed_engine(PHILOX, 13), 777)
+    assert np.array_equal(host(u), golden_arrays["burn__philox_uniform_f64_m1p1_777"])
+
+
+# ------------------------------------------------- alignment / lane shifts
+
+
+@pytest.mark.parametrize("dist,prec", [("bits", "fp32"), ("uniform", "fp32"), ("uniform", "fp64"),
+                                       ("gaussian", "fp32"), ("gaussian", "fp64"), ("lognormal", "fp32")])
+def test_every_lane_and_output_offset(dist, prec):
+    """Start lane 0..3 x output offset 0..7 elements exercises the aligned,
+    funnel-shift and scalar paths of the Philox kernel."""
+    key = (0xCAFEF00D, 0x12345678)
+    n = 4099
+    dtype = {"bits": torch.uint32, "fp32": torch.float32, "fp64": torch.float64}["bits" if dist == "bits" else prec]
+    for lane in range(4):
+        for skip_blocks in (0, 1, (1 << 32) - 1):
+            pos = 4 * skip_blocks + lane
+            st = P.engine._state_at(key, pos)
+            want = O.generate("philox", (key, pos), dist, n, prec, -3.0 if dist == "uniform" else 0.5,
+                              5.0 if dist == "uniform" else 1.5)
+            for off in range(8):
+                buf = torch.full((n + 16,), 7, dtype=dtype, device="cuda")
+                out = buf[off:off + n]
+                spec = spec_for(dist, prec, -3.0 if dist == "uniform" else 0.5, 5.0 if dist == "uniform" else 1.5)
+                P.generate(spec, st, n, out=out)
+                hb = host(buf)
+                compare(dist, prec, hb[off:off + n], want, spec_p0(spec), spec_p1(spec), "fast",
+                        f"lane{lane} blk{skip_blocks} off{off}")
+                # no writes outside the slice
+                assert np.all(hb[:off] == 7) and np.all(hb[off + n:] == 7)
+
+
+def spec_p0(spec):
+    return getattr(spec, "mean", getattr(spec, "m", getattr(spec, "lo", 0.0)))
+
+
+def spec_p1(spec):
+    return getattr(spec, "stddev", getattr(spec, "s", getattr(spec, "hi", 0.0)))
+
+
+def test_counter_carry_across_all_lanes():
+    key = (1, 2)
+    for ctr in ((0xFFFFFFFF, 0, 0, 0), (0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 0), (0xFFFFFFFF,) * 4):
+        for lane in range(4):
+            st = P.PhiloxState(key, ctr, lane_index=4)
+            st = P.skip_ahead(st, lane) if lane else st
+            pos = P.stream_position(st)
+            got = host(P.generate_words(st, 40)[1])
+            assert np.array_equal(got, O.philox_words(key, pos, 40))
+
+
+# --------------------------------------------------- MRG32k3a jump-ahead
+
+
+def test_mrg_jump_ahead_slices_equal_sequential_stream():
+    s1, s2 = O.seed_mrg(777)
+    n = 1 << 22
+    want = O.mrg_fill(*s1, *s2, n)[0]
+    got = host(P.generate(P.UniformBits(), P.seed_engine(MRG, 777), n)[1])
+    assert np.array_equal(got, want)
+    # slices started from skip_ahead states == slices of the single stream
+    base = P.seed_engine(MRG, 777)
+    for start, cnt in ((1, 5), (4095, 70000), (1234567, 3), (n - 1000, 1000)):
+        got = host(P.generate(P.UniformBits(), P.skip_ahead(base, start), cnt)[1])
+        assert np.array_equal(got, want[start:start + cnt]), (start, cnt)
+
+
+def test_mrg_c2_full_size_spot_windows():
+    """C2 at n=2^28: fp64 uniform on [-123.456, 987.654); spot windows across
+    every thread chunk boundary region vs the oracle stream at the same offsets."""
+    n = 1 << 28
+    base = P.seed_engine(MRG, 777)
+    _, out = P.generate(P.Uniform(-123.456, 987.654, "fp64"), base, n)
+    s1, s2 = O.seed_mrg(777)
+    rng = np.random.default_rng(5)
+    starts = sorted(set([0, n - 4096] + [int(x) for x in rng.integers(0, n - 4096, 24)]))
+    for st in starts:
+        j1, j2 = O.mrg_skip(s1, s2, st)
+        w = O.mrg_fill(*j1, *j2, 4096)[0]
+        want = O.range_transform(O.words_to_unit(w, "fp64"), -123.456, 987.654)
+        assert np.array_equal(host(out[st:st + 4096]), want), st
+    v = out
+    assert float(v.min()) >= -123.456 and float(v.max()) < 987.654
+
+
+# ----------------------------------------------------- large-size properties
+
+
+def test_c4_sharded_slices_concatenate_to_single_stream():
+    base = P.seed_engine(PHILOX, 777)
+    n = (1 << 26) + 12
+    _, full = P.generate(P.Uniform(0.0, 1.0), base, n)
+    from paper_2109_01329_b200.sharding import generate_shard, strong_shard
+
+    for world in (2, 3, 8):
+        parts = [generate_shard(P.Uniform(0.0, 1.0), base, strong_shard(n, r, world)) for r in range(world)]
+        assert torch.equal(torch.cat(parts), full)
+
+
+def test_c3_gaussian_2p30_statistics_and_spot_parity():
+    n = 1 << 30
+    base = P.seed_engine(PHILOX, 777)
+    _, z = P.generate(P.Gaussian(0.0, 1.0), base, n)
+    zz = z.double()
+    assert abs(float(zz.mean())) < 2e-4
+    assert abs(float(zz.std()) - 1.0) < 2e-4
+    key = O.seed_philox(777)
+    for st in (0, 2 * 12345679, n - 2048):
+        want = O.generate("philox", (key, st), "gaussian", 2048, "fp32", 0.0, 1.0)
+        check_close(host(z[st:st + 2048]), want, gaussian_allowed(want, 0.0, 1.0, np.float32, True), f"c3@{st}")
+    del z, zz
+    _, x = P.generate(P.Lognormal(0.0, 1.0), base, n)
+    for st in (0, n - 2048):
+        want = O.generate("philox", (key, st), "lognormal", 2048, "fp32", 0.0, 1.0)
+        check_close(host(x[st:st + 2048]), want, lognormal_allowed(want, 0.0, 1.0, np.float32, True), f"ln@{st}")
+    assert float(x.min()) > 0
+
+
+def test_uniform_2p32_bounds_and_window():
+    n = 1 << 32
+    base = P.seed_engine(PHILOX, 777)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    P.generate(P.Uniform(0.0, 1.0), base, n, out=out)
+    assert float(out.min()) >= 0.0 and float(out.max()) < 1.0
+    key = O.seed_philox(777)
+    for st in (0, (1 << 31) + 4, n - 1024):
+        want = O.words_to_unit(O.philox_words(key, st, 1024), "fp32")
+        assert np.array_equal(host(out[st:st + 1024]), want)
+
+
+# ------------------------------------------------------- other entry points
+
+
+def test_kernels_dropin_matches_reference_kernel_tests():
+    from paper_2109_01329_b200 import _kernels as K
+
+    assert K.IMPL == "cuda"
+    key = (0xCAFEF00D, 0x12345678)
+    for offset, n in [(0, 1), (0, 4), (1, 9), (3, 2), (2, 4097)]:
+        w = K.philox_fill(key[0], key[1], 0, 0, 0, 0, offset, n)
+        assert w.dtype == np.uint32 and np.array_equal(w, O.philox_fill(*key, 0, 0, 0, 0, offset, n))
+    args = (1, 2, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 0, 2, 20)
+    assert np.array_equal(K.philox_fill(*args), O.philox_fill(*args))
+    a, a1, a2 = K.mrg_fill(*(12345,) * 6, 5000)
+    f, f1, f2 = O.mrg_fill(*(12345,) * 6, 5000)
+    assert np.array_equal(a, f) and a1 == f1 and a2 == f2
+    rng = np.random.default_rng(23)
+    u1 = 1.0 - rng.integers(0, 2**24, 20000).astype(np.float64) / 2**24
+    u2 = rng.integers(0, 2**24, 20000).astype(np.float64) / 2**24
+    c0, c1 = K.box_muller(u1, u2)
+    o0, o1 = O.box_muller(u1, u2)
+    # test_kernels.py:58-67 tolerance between two libm-grade implementations
+    assert np.allclose(c0, o0, rtol=1e-13, atol=1e-13) and np.allclose(c1, o1, rtol=1e-13, atol=1e-13)
+
+
+def test_kernels_dropin_large_chunked():
+    from paper_2109_01329_b200 import _kernels as K
+
+    n = (1 << 26) + 77  # crosses the library's host staging chunk
+    w = K.philox_fill(5, 6, 0xFFFFFFF0, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 3, n)
+    assert np.array_equal(w, O.philox_fill(5, 6, 0xFFFFFFF0, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF, 3, n))
+    m, s1, s2 = K.mrg_fill(*(777,) * 6, n)
+    om, o1, o2 = O.mrg_fill(*(777,) * 6, n)
+    assert np.array_equal(m, om) and s1 == o1 and s2 == o2
+
+
+def test_words_to_unit_and_range_transform():
+    st = P.seed_engine(PHILOX, 99)
+    _, words = P.generate_words(st, 10001)
+    key = O.seed_philox(99)
+    ow = O.philox_words(key, 0, 10001)
+    for prec in ("fp32", "fp64"):
+        u = P.words_to_unit(words, prec)
+        assert np.array_equal(host(u), O.words_to_unit(ow, prec))
+        blk = P.RandomBlock(u, 10001, prec)
+        P.range_transform(blk, -123.456, 987.654)
+        want = O.range_transform(O.words_to_unit(ow, prec), -123.456, 987.654)
+        assert np.array_equal(host(blk.values), want)
+
+
+def test_gaussian_from_words():
+    _, words = P.generate_words(P.seed_engine(PHILOX, 5), 2000)
+    ow = O.philox_words(O.seed_philox(5), 0, 2000)
+    for prec, method in (("fp64", "accurate"), ("fp32", "fast"), ("fp32", "accurate")):
+        got = host(P.gaussian_from_words(words, 7.0, 2.5, 1999, prec, method))
+        want = O.gaussian_from_words(ow, 7.0, 2.5, 1999, prec)
+        dt = np.float32 if prec == "fp32" else np.float64
+        check_close(got, want, gaussian_allowed(want, 7.0, 2.5, dt, method == "fast"), prec + method)
+
+
+def test_segments_kernel_matches_per_batch_requests():
+    """C5 shape: many batches at chained offsets in one launch."""
+    from paper_2109_01329_b200 import calosim
+
+    key = O.seed_philox(777)
+    counts = [200000, 200003, 1, 5, 19999, 200000]
+    table = calosim.segment_table(start_position=3, counts=counts)
+    out = torch.empty(sum(counts) + 64, dtype=torch.float32, device="cuda")
+    calosim.generate_segments(P.seed_engine(PHILOX, 777), table, out)
+    pos, off = 3, 0
+    ho = host(out)
+    for c in counts:
+        want = O.words_to_unit(O.philox_words(key, pos, c), "fp32")
+        assert np.array_equal(ho[off:off + c], want)
+        pos += c
+        off += c
+
+
+# ------------------------------------------------------------ errors
+
+
+def test_error_behaviour_matches_reference():
+    st = P.seed_engine(PHILOX, 1)
+    with pytest.raises(P.InvalidRange):
+        P.Uniform(1.0, 1.0)
+    with pytest.raises(P.InvalidParameter):
+        P.Gaussian(0.0, 0.0)
+    with pytest.raises(P.InvalidParameter):
+        P.Uniform(0.0, 1.0, precision="fp16")
+    with pytest.raises(ValueError):
+        P.generate_words(st, -1)
+    with pytest.raises(ValueError):
+        P.skip_ahead(st, -1)
+    blk = P.RandomBlock(torch.zeros(4, device="cuda"), 4)
+    with pytest.raises(P.InvalidRange):
+        P.range_transform(blk, 0.0, float("inf"))
+    # wrong dtype / host tensor for out
+    with pytest.raises(P.InvalidParameter):
+        P.generate(P.Uniform(0.0, 1.0), st, 4, out=torch.zeros(4, dtype=torch.float64, device="cuda"))
+    with pytest.raises(P.InvalidParameter):
+        P.generate(P.Uniform(0.0, 1.0), st, 4, out=torch.zeros(4))
+    # empty request: no launch, state unchanged
+    new, out = P.generate(P.Uniform(0.0, 1.0), st, 0)
+    assert new is st and out.numel() == 0
+
+
+def test_state_round_trip_matches_reference_accounting():
+    st = P.seed_engine(PHILOX, 8)
+    assert P.stream_position(st) == 0
+    s2, _ = P.generate_words(st, 37)
+    assert P.stream_position(s2) == 37
+    s5, b5 = P.fill_gaussian(st, 5, 0.0, 1.0)
+    s6, b6 = P.fill_gaussian(st, 6, 0.0, 1.0)
+    assert P.stream_position(s5) == 6 == P.stream_position(s6)
+    assert torch.equal(b5.values, b6.values[:5])
+    # next_word (device-computed) streams the KAT lanes in order
+    s = P.seed_engine(PHILOX, 0)
+    words = []
+    for _ in range(4):
+        s, w = P.next_word(s)
+        words.append(w)
+    assert tuple(words) == (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)
