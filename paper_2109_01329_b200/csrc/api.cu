@@ -686,15 +686,16 @@ int prng_kernels_philox_fill(uint32_t k0, uint32_t k1, uint32_t b0, uint32_t b1,
     const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
     int rc = scratch(chunk * 4, &d, &s);
     if (rc) return rc;
-    // position of the first word; each chunk restarts from its own offset
-    // exactly as the reference's chunk kernels do (rngburn.py:70-73).
-    u128 pos = (((u128)b3 << 96) | ((u128)b2 << 64) | ((u128)b1 << 32) | b0) * 4 + offset;
+    // Each chunk restarts from its own stream offset exactly as the
+    // reference's chunk kernels do (rngburn.py:70-73); the block counter
+    // wraps mod 2^128 like _core.pyx:63-70.
+    const u128 base_blk = ((u128)b3 << 96) | ((u128)b2 << 64) | ((u128)b1 << 32) | b0;
     for (uint64_t done = 0; done < n; done += chunk) {
         const uint64_t m = (n - done) < chunk ? (n - done) : chunk;
-        const u128 p = pos + done;
-        const u128 blk = p >> 2;
+        const uint64_t rel = (uint64_t)offset + done;
+        const u128 blk = base_blk + (rel >> 2);
         const uint32_t ctr[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)(blk >> 64), (uint32_t)(blk >> 96)};
-        rc = launch_philox<kBits>(k0, k1, ctr, (uint32_t)(p & 3), m, d, XformParams{}, s);
+        rc = launch_philox<kBits>(k0, k1, ctr, (uint32_t)(rel & 3), m, d, XformParams{}, s);
         if (rc) return rc;
         PRNG_CUDA(cudaMemcpyAsync(host_out + done, d, m * 4, cudaMemcpyDeviceToHost, s));
     }
