@@ -25,6 +25,8 @@ static_assert(sizeof(prng_segment_t) == sizeof(PhiloxSegment), "segment layout")
 
 namespace {
 
+typedef unsigned __int128 u128;
+
 thread_local char g_err[512] = "";
 
 int fail(int code, const char* fmt, ...) {
@@ -179,10 +181,13 @@ template <typename T>
 int launch_range(T* v, uint64_t n, double lo, double hi, void* stream);
 
 // ---- Philox launch ----
+// Plan: scalar head (to a 32-byte boundary) + body groups + scalar tail; the
+// body is cut into launches inside which c1..c3 are constant (philox.cuh).
 template <int X>
 int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, uint64_t n, void* out,
                   const XformParams& p, void* stream) {
     using T = typename XformTraits<X>::T;
+    constexpr bool kPair = XformTraits<X>::kPair;
     if (n == 0) return PRNG_OK;
     if (ctr == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "ctr must not be NULL");
     if (lane > 3) return fail(PRNG_ERR_INVALID_PARAMETER, "lane must be 0..3, got %u", lane);
@@ -192,44 +197,73 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
     int rc = bind_output(out, &dptr);
     if (rc) return rc;
 
-    PhiloxLaunch a{};
-    a.k0 = k0;
-    a.k1 = k1;
-    a.ctr_lo = (uint64_t)ctr[0] | ((uint64_t)ctr[1] << 32);
-    a.ctr_hi = (uint64_t)ctr[2] | ((uint64_t)ctr[3] << 32);
-    a.lane = lane;
-    a.n = n;
-    a.out = dptr;
-    a.p = p;
-    const int shift = plan_philox(a, (uint64_t)(uintptr_t)dptr, sizeof(T), XformTraits<X>::kPair);
-
-    const void* kern;
-    uint64_t threads;
-    switch (shift) {
-        case 0:
-            kern = (const void*)philox_kernel<X, 0>;
-            threads = sizeof(T) == 4 ? (a.ngroups + 1) / 2 : a.ngroups;
-            break;
-        case 1: kern = (const void*)philox_kernel<X, 1>; threads = (a.ngroups + 30) / 31 * 32; break;
-        case 2: kern = (const void*)philox_kernel<X, 2>; threads = (a.ngroups + 30) / 31 * 32; break;
-        default: kern = (const void*)philox_kernel<X, 3>; threads = (a.ngroups + 30) / 31 * 32; break;
+    PhiloxScalar s{};
+    s.k0 = k0;
+    s.k1 = k1;
+    s.ctr_lo = (uint64_t)ctr[0] | ((uint64_t)ctr[1] << 32);
+    s.ctr_hi = (uint64_t)ctr[2] | ((uint64_t)ctr[3] << 32);
+    s.lane = lane;
+    s.n = n;
+    uint64_t i0 = ((32u - (uint32_t)((uintptr_t)dptr & 31u)) & 31u) / sizeof(T);
+    uint64_t ngroups = 0;
+    if ((kPair && (i0 & 1)) || i0 >= n) {
+        i0 = n;  // misaligned for pairs (or tiny): everything scalar
+    } else {
+        ngroups = (n - i0) >> 2;
     }
-    const uint64_t nscalar = a.i0 + (a.n - a.i0 - 4 * a.ngroups);
-    if (nscalar > threads) threads = nscalar;
+    s.i0 = i0;
+    s.tail0 = i0 + 4 * ngroups;
+    const int shift = (int)((lane + i0) & 3);
+    const void* kern = shift == 0   ? (const void*)philox_kernel<X, 0>
+                       : shift == 1 ? (const void*)philox_kernel<X, 1>
+                       : shift == 2 ? (const void*)philox_kernel<X, 2>
+                                    : (const void*)philox_kernel<X, 3>;
     int sms = 0, occ = 0;
     rc = resident_ctas(kern, kPhiloxThreads, &sms, &occ);
     if (rc) return rc;
-    uint64_t blocks = (threads + kPhiloxThreads - 1) / kPhiloxThreads;
     const uint64_t cap = (uint64_t)sms * occ;
-    if (blocks > cap) blocks = cap;
-    if (blocks < 1) blocks = 1;
-    void* args[] = {&a};
-    PRNG_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(kPhiloxThreads), args, 0, (cudaStream_t)stream));
+
+    u128 blk = (((u128)s.ctr_hi << 64) | s.ctr_lo) + ((lane + i0) >> 2);
+    T* body = static_cast<T*>(dptr) + i0;
+    uint64_t left = ngroups;
+    bool first = true;
+    do {
+        const uint32_t c0 = (uint32_t)blk;
+        uint64_t g = (1ull << 32) - c0;
+        if (g > left) g = left;
+        if (g > (1ull << 31)) g = 1ull << 31;
+        // A launch boundary at an odd group leaves the next body 16-byte
+        // aligned; emit one single-group launch to restore 32-byte alignment
+        // for the 256-bit stores (rare: only at 2^34-word stream boundaries).
+        if (left > 0 && ((uintptr_t)body & 31u) != 0) g = 1;
+        PhiloxBody a{};
+        a.k0 = k0;
+        a.k1 = k1;
+        a.c0 = c0;
+        a.c1 = (uint32_t)(blk >> 32);
+        a.c2 = (uint32_t)(blk >> 64);
+        a.c3 = (uint32_t)(blk >> 96);
+        a.ngroups = (uint32_t)g;
+        a.out = body;
+        a.p = p;
+        if (first) a.s = s;  // head/tail ride on the first launch
+        uint64_t threads = shift == 0 ? (g + PhiloxBpt<T>::kValue - 1) / PhiloxBpt<T>::kValue : (g + 30) / 31 * 32;
+        const uint64_t nscalar = first ? s.i0 + (n - s.tail0) : 0;
+        if (nscalar > threads) threads = nscalar;
+        uint64_t blocks = (threads + kPhiloxThreads - 1) / kPhiloxThreads;
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        void* args[] = {&a};
+        PRNG_CUDA(cudaLaunchKernel(kern, dim3((unsigned)blocks), dim3(kPhiloxThreads), args, 0, (cudaStream_t)stream));
+        blk += g;
+        body += 4 * g;
+        left -= g;
+        first = false;
+    } while (left > 0);
     return PRNG_OK;
 }
 
 // ---- MRG32k3a host math: jump matrices A^k mod m ----
-typedef unsigned __int128 u128;
 struct Mat3 {
     uint64_t v[9];
 };

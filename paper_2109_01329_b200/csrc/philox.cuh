@@ -1,48 +1,62 @@
-// philox.cuh -- fused Philox4x32-10 generate+transform kernel (sm_100a).
+// philox.cuh -- fused Philox4x32-10 generate+transform kernels (sm_100a).
 //
 // Replaces the reference hot loop _core.pyx:42-71 (philox_fill) together with
-// the two passes layered on it: words_to_unit (distributions.py:83-87) and the
-// range transform (distributions.py:98-104 / rngburn.py:62-64, 94-100), or
-// Box-Muller (distributions.py:116-131) / lognormal.  Each sample is written
-// to HBM exactly once.
+// the passes layered on it: words_to_unit (distributions.py:83-87), the range
+// transform (distributions.py:98-104 / rngburn.py:62-64, 94-100), Box-Muller
+// (distributions.py:116-131) and the lognormal extension.  Each sample is
+// written to HBM exactly once.
 //
-// Work decomposition.  A request is n elements starting at stream word
-// `lane` of the block with 128-bit counter `ctr` (the reference's
-// philox_fill(k0, k1, b0..b3, offset, n) arguments, engine.py:222-225).
-// Output element i consumes "virtual word" v = lane + i, i.e. lane v&3 of
-// block ctr + (v>>2).  The output is split into
+// Work decomposition.  A request is n elements starting at stream word `lane`
+// of the block with 128-bit counter `ctr` (the reference's philox_fill(k0, k1,
+// b0..b3, offset, n) arguments, engine.py:222-225).  Output element i consumes
+// "virtual word" v = lane + i, i.e. lane v&3 of block ctr + (v>>2).  The
+// output is split into
 //   * a scalar head [0, i0) that brings out+i0 to a 32-byte boundary,
-//   * a body of `ngroups` 4-element groups, group g holding virtual words
+//   * a body of 4-element groups, group g holding virtual words
 //     lane+i0+4g .. +3, stored with 128/256-bit streaming stores,
 //   * a scalar tail.
-// When (lane + i0) % 4 == 0 every body group is exactly one Philox block
-// (SHIFT = 0): each thread computes two adjacent blocks and issues one
-// 256-bit store (fp32/u32) or one 256-bit store per block (fp64), so a warp
-// instruction writes 1 KiB of contiguous output.  Otherwise (SHIFT = 1..3) a
-// group straddles two blocks: lane t of a warp computes block t and takes the
-// first SHIFT words of block t+1 from lane t+1 by shuffle; each warp pass
-// emits 31 groups from 32 blocks.
+// The host cuts the body into launches inside which the upper 96 counter bits
+// are constant (a new launch at every 2^32-block boundary, i.e. every 2^34
+// words): c1..c3 are then kernel-uniform, the per-block counter is one 32-bit
+// add, and the first two Philox rounds partly fold into uniform registers.
+// When (lane + i0) % 4 == 0 every group is exactly one Philox block
+// (SHIFT = 0): a thread computes BPT adjacent blocks and issues 256-bit
+// stores.  Otherwise (SHIFT = 1..3) a group straddles two blocks: lane t of a
+// warp computes block t and takes the first SHIFT words of block t+1 from lane
+// t+1 by shuffle; each warp pass emits 31 groups from 32 blocks.
 #pragma once
 
 #include "common.cuh"
 
 namespace prng {
 
-struct PhiloxLaunch {
+constexpr int kPhiloxThreads = 256;
+
+// Scalar (head / tail / fully generic) description of a request.
+struct PhiloxScalar {
     uint32_t k0, k1;
     uint64_t ctr_lo, ctr_hi;  // counter of the block holding element 0
-    uint32_t lane;            // virtual word index of element 0 (0..3)
-    uint64_t n;               // elements
-    uint64_t i0;              // scalar head length
-    uint64_t ngroups;         // vector body groups
-    uint64_t body_blk;        // (lane + i0) >> 2
-    void* out;
+    uint32_t lane;            // virtual word of element 0 (0..3)
+    uint64_t i0;              // head length
+    uint64_t tail0;           // first tail element
+    uint64_t n;               // total elements
+};
+
+// One body launch: `ngroups` groups whose first block has counter
+// (c0, c1, c2, c3), with c0 + ngroups (+1 for SHIFT > 0) <= 2^32.
+struct PhiloxBody {
+    uint32_t k0, k1;
+    uint32_t c0, c1, c2, c3;
+    uint32_t ngroups;
+    void* out;  // address of group 0
     XformParams p;
+    PhiloxScalar s;  // head/tail done by this launch when s.n != 0
 };
 
 // Element i computed on its own (head, tail and the fully generic path).
 template <int X>
-__device__ __forceinline__ typename XformTraits<X>::T philox_scalar(const PhiloxLaunch& a, uint64_t i) {
+__device__ __forceinline__ typename XformTraits<X>::T philox_scalar(const PhiloxScalar& a, const XformParams& p,
+                                                                    uint64_t i) {
     using T = typename XformTraits<X>::T;
     if constexpr (XformTraits<X>::kPair) {
         const uint64_t v0 = a.lane + 2 * (i >> 1);
@@ -55,12 +69,24 @@ __device__ __forceinline__ typename XformTraits<X>::T philox_scalar(const Philox
             w1 = lane_of(b, (uint32_t)(v0 & 3) + 1);
         }
         T o0, o1;
-        xform2<X>(w0, w1, a.p, o0, o1);
+        xform2<X>(w0, w1, p, o0, o1);
         return (i & 1) ? o1 : o0;
     } else {
         const uint64_t v = a.lane + i;
         const U4 b = philox_block(a.k0, a.k1, counter_add(a.ctr_lo, a.ctr_hi, v >> 2));
-        return xform1<X>(lane_of(b, (uint32_t)(v & 3)), a.p);
+        return xform1<X>(lane_of(b, (uint32_t)(v & 3)), p);
+    }
+}
+
+template <int X>
+__device__ __forceinline__ void philox_scalar_range(const PhiloxScalar& a, const XformParams& p, void* out_base,
+                                                    uint64_t gtid, uint64_t gstride) {
+    using T = typename XformTraits<X>::T;
+    T* out = static_cast<T*>(out_base);
+    const uint64_t nscalar = a.i0 + (a.n - a.tail0);
+    for (uint64_t s = gtid; s < nscalar; s += gstride) {
+        const uint64_t i = s < a.i0 ? s : a.tail0 + (s - a.i0);
+        out[i] = philox_scalar<X>(a, p, i);
     }
 }
 
@@ -72,77 +98,57 @@ __device__ __forceinline__ U4 funnel(const U4& a, const U4& b) {
     return a;
 }
 
-constexpr int kPhiloxThreads = 256;
-
-// Split a request into head / body / tail for an output at `out_addr`.
-// Returns the body SHIFT ((lane + i0) & 3).  Pair transforms need the body to
-// start on a pair boundary (i0 even); if the output is misaligned for that
-// (fp32 at an odd 4-byte offset) everything goes through the scalar path.
-__host__ __device__ inline int plan_philox(PhiloxLaunch& a, uint64_t out_addr, uint32_t esize, bool pair) {
-    const uint64_t i0 = ((32u - (uint32_t)(out_addr & 31u)) & 31u) / esize;
-    if ((pair && (i0 & 1)) || i0 >= a.n) {
-        a.i0 = a.n;
-        a.ngroups = 0;
-        a.body_blk = 0;
-        return 0;
-    }
-    a.i0 = i0;
-    a.ngroups = (a.n - i0) >> 2;
-    a.body_blk = (a.lane + i0) >> 2;
-    return (int)((a.lane + i0) & 3);
-}
+// Blocks per thread per pass on the aligned path: 4 for 4-byte outputs (two
+// 256-bit stores of 64 contiguous bytes), 2 for 8-byte outputs.
+template <typename T> struct PhiloxBpt { static constexpr int kValue = 4; };
+template <> struct PhiloxBpt<double> { static constexpr int kValue = 2; };
 
 template <int X, int SHIFT>
-__device__ __forceinline__ void philox_body(const PhiloxLaunch& a, uint64_t gtid, uint64_t gstride) {
+__device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, uint32_t gstride) {
     using T = typename XformTraits<X>::T;
-    T* __restrict__ out = static_cast<T*>(a.out);
-
-    // Scalar head/tail (at most 7 + 3 elements unless the request is
-    // misaligned for pair transforms, in which case everything is scalar).
-    const uint64_t body_end = a.i0 + 4 * a.ngroups;
-    const uint64_t nscalar = a.i0 + (a.n - body_end);
-    for (uint64_t s = gtid; s < nscalar; s += gstride) {
-        const uint64_t i = s < a.i0 ? s : body_end + (s - a.i0);
-        out[i] = philox_scalar<X>(a, i);
-    }
-    if (a.ngroups == 0) return;
-    T* __restrict__ body = out + a.i0;
-
+    T* __restrict__ body = static_cast<T*>(a.out);
     if constexpr (SHIFT == 0) {
-        if constexpr (sizeof(T) == 4) {
-            // Two blocks per thread -> one 256-bit store.
-            const uint64_t nunits = (a.ngroups + 1) >> 1;
-            for (uint64_t u = gtid; u < nunits; u += gstride) {
-                const uint64_t g = 2 * u;
-                const U4 w0 = philox_block(a.k0, a.k1, counter_add(a.ctr_lo, a.ctr_hi, a.body_blk + g));
-                T o0[4];
-                xform4<X>(w0, a.p, o0);
-                if (g + 1 < a.ngroups) {
-                    const U4 w1 = philox_block(a.k0, a.k1, counter_add(a.ctr_lo, a.ctr_hi, a.body_blk + g + 1));
-                    T o1[4];
-                    xform4<X>(w1, a.p, o1);
-                    st_group2(body + 4 * g, o0, o1);
-                } else {
-                    st_group(body + 4 * g, o0);
-                }
+        constexpr int BPT = PhiloxBpt<T>::kValue;
+        const uint32_t nunits = (a.ngroups + BPT - 1) / BPT;
+        for (uint32_t u = gtid; u < nunits; u += gstride) {
+            const uint32_t g0 = u * BPT;
+            T o[BPT][4];
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) {
+                const U4 w = philox_block(a.k0, a.k1, U4{a.c0 + g0 + j, a.c1, a.c2, a.c3});
+                xform4<X>(w, a.p, o[j]);
             }
-        } else {
-            for (uint64_t g = gtid; g < a.ngroups; g += gstride) {
-                const U4 w = philox_block(a.k0, a.k1, counter_add(a.ctr_lo, a.ctr_hi, a.body_blk + g));
-                T o[4];
-                xform4<X>(w, a.p, o);
-                st_group(body + 4 * g, o);
+            T* dst = body + (size_t)4 * g0;
+            if (g0 + BPT <= a.ngroups) {
+                if constexpr (sizeof(T) == 4) {
+#pragma unroll
+                    for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BPT; ++j) st_group(dst + 4 * j, o[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < BPT; ++j)
+                    if (g0 + j < a.ngroups) st_group(dst + 4 * j, o[j]);
             }
         }
     } else {
         // Warp-cooperative funnel: 32 blocks -> 31 groups per pass.
         const uint32_t lane = threadIdx.x & 31;
-        const uint64_t gwarp = gtid >> 5;
-        const uint64_t nwarps = gstride >> 5;
-        const uint64_t ntiles = (a.ngroups + 30) / 31;
-        for (uint64_t tile = gwarp; tile < ntiles; tile += nwarps) {
-            const uint64_t g = tile * 31 + lane;
-            const U4 w = philox_block(a.k0, a.k1, counter_add(a.ctr_lo, a.ctr_hi, a.body_blk + g));
+        const uint32_t gwarp = gtid >> 5;
+        const uint32_t nwarps = gstride >> 5;
+        const uint32_t ntiles = (uint32_t)(((uint64_t)a.ngroups + 30) / 31);
+        for (uint32_t tile = gwarp; tile < ntiles; tile += nwarps) {
+            const uint32_t g = tile * 31 + lane;
+            // The block after a launch's last group may sit past a 2^32
+            // boundary of c0: carry into the upper words (rare, predicated).
+            U4 c{a.c0 + g, a.c1, a.c2, a.c3};
+            if (c.x < a.c0) {
+                c.y += 1;
+                if (c.y == 0 && ++c.z == 0) ++c.w;
+            }
+            const U4 w = philox_block(a.k0, a.k1, c);
             U4 nx;
             nx.x = __shfl_down_sync(0xffffffffu, w.x, 1);
             nx.y = __shfl_down_sync(0xffffffffu, w.y, 1);
@@ -151,19 +157,28 @@ __device__ __forceinline__ void philox_body(const PhiloxLaunch& a, uint64_t gtid
             if (lane < 31 && g < a.ngroups) {
                 T o[4];
                 xform4<X>(funnel<SHIFT>(w, nx), a.p, o);
-                st_group(body + 4 * g, o);
+                st_group(body + (size_t)4 * g, o);
             }
         }
     }
 }
 
 template <int X, int SHIFT>
-__global__ void __launch_bounds__(kPhiloxThreads) philox_kernel(const PhiloxLaunch a) {
-    philox_body<X, SHIFT>(a, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, (uint64_t)gridDim.x * blockDim.x);
+__global__ void __launch_bounds__(kPhiloxThreads) philox_kernel(const PhiloxBody a) {
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t gstride = gridDim.x * blockDim.x;
+    if (a.s.n) {
+        using T = typename XformTraits<X>::T;
+        philox_scalar_range<X>(a.s, a.p, static_cast<T*>(a.out) - a.s.i0, gtid, gstride);
+    }
+    if (a.ngroups) philox_body<X, SHIFT>(a, gtid, gstride);
 }
 
-// Segment table (many small batches in one launch): blockIdx.y strides over
-// segments, blockIdx.x over each segment's elements.
+// ------------------------------------------------------------- segments
+// Many small requests in one launch (FastCaloSim consumer): blockIdx.y
+// strides over segments, blockIdx.x over each segment's groups.  Segments
+// keep the generic 64-bit counter arithmetic since a segment may straddle a
+// 2^32-block boundary.
 struct PhiloxSegment {
     uint64_t pos_lo, pos_hi, count, out_offset;
 };
@@ -173,11 +188,12 @@ __global__ void __launch_bounds__(kPhiloxThreads)
     philox_segments_kernel(uint32_t k0, uint32_t k1, const PhiloxSegment* __restrict__ segs, uint32_t nseg,
                            XformParams p, typename XformTraits<X>::T* out) {
     using T = typename XformTraits<X>::T;
+    static_assert(!XformTraits<X>::kPair, "segments carry single-word transforms only");
     const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
     for (uint32_t s = blockIdx.y; s < nseg; s += gridDim.y) {
         const PhiloxSegment sg = segs[s];
-        PhiloxLaunch a;
+        PhiloxScalar a;
         a.k0 = k0;
         a.k1 = k1;
         // block = pos >> 2 (128-bit), lane = pos & 3 (engine.py:221-222)
@@ -185,14 +201,31 @@ __global__ void __launch_bounds__(kPhiloxThreads)
         a.ctr_hi = sg.pos_hi >> 2;
         a.lane = (uint32_t)(sg.pos_lo & 3);
         a.n = sg.count;
-        a.out = out + sg.out_offset;
-        a.p = p;
-        const int shift = plan_philox(a, (uint64_t)(uintptr_t)a.out, sizeof(T), XformTraits<X>::kPair);
-        switch (shift) {
-            case 0: philox_body<X, 0>(a, gtid, gstride); break;
-            case 1: philox_body<X, 1>(a, gtid, gstride); break;
-            case 2: philox_body<X, 2>(a, gtid, gstride); break;
-            default: philox_body<X, 3>(a, gtid, gstride); break;
+        T* dst = out + sg.out_offset;
+        // head to a 16-byte boundary, 4-element groups, tail
+        const uint64_t mis = ((16u - (uint32_t)((uintptr_t)dst & 15u)) & 15u) / sizeof(T);
+        const uint64_t i0 = mis < a.n ? mis : a.n;
+        const uint64_t ng = (a.n - i0) >> 2;
+        a.i0 = i0;
+        a.tail0 = i0 + 4 * ng;
+        const uint64_t nscalar = i0 + (a.n - a.tail0);
+        for (uint64_t q = gtid; q < nscalar; q += gstride) {
+            const uint64_t i = q < i0 ? q : a.tail0 + (q - i0);
+            dst[i] = philox_scalar<X>(a, p, i);
+        }
+        const uint64_t v0 = a.lane + i0;  // virtual word of group 0
+        const uint32_t shift = (uint32_t)(v0 & 3);
+        for (uint64_t g = gtid; g < ng; g += gstride) {
+            const uint64_t v = v0 + 4 * g;
+            const U4 b0 = philox_block(k0, k1, counter_add(a.ctr_lo, a.ctr_hi, v >> 2));
+            U4 w = b0;
+            if (shift) {
+                const U4 b1 = philox_block(k0, k1, counter_add(a.ctr_lo, a.ctr_hi, (v >> 2) + 1));
+                w = shift == 1 ? funnel<1>(b0, b1) : shift == 2 ? funnel<2>(b0, b1) : funnel<3>(b0, b1);
+            }
+            T o[4];
+            xform4<X>(w, p, o);
+            st_group(dst + i0 + 4 * g, o);
         }
     }
 }
