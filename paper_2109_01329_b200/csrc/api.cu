@@ -244,6 +244,7 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
         a.c2 = (uint32_t)(blk >> 64);
         a.c3 = (uint32_t)(blk >> 96);
         a.ngroups = (uint32_t)g;
+        a.pre = philox_pre(k0, k1, a.c1, a.c2, a.c3);
         a.out = body;
         a.p = p;
         if (first) a.s = s;  // head/tail ride on the first launch

@@ -55,6 +55,63 @@ __device__ __forceinline__ U4 philox_block(uint32_t k0, uint32_t k1, U4 c) {
     return c;
 }
 
+// Rounds 1-3 with the upper counter words (c1, c2, c3) uniform across the
+// launch: everything that depends only on (key, c1, c2, c3) is folded on the
+// host into five words, so a block costs 18 vector IMAD.WIDE instead of 20 and
+// no uniform->vector moves (philox.cuh, "PhiloxBody").
+struct PhiloxPre {
+    uint32_t r1_x3;  // c3 ^ k1                      (round 1: c2' = hi(M0 c0) ^ r1_x3)
+    uint32_t r2_x1;  // lo(M1 c2) ^ (k0 + W0)        (round 2: c0'' = hi(M1 c2') ^ r2_x1)
+    uint32_t r2_x3;  // hi(M0 U0) ^ (k1 + W1)        (round 2: c2'' = lo(M0 c0) ^ r2_x3)
+    uint32_t r2_c3;  // lo(M0 U0), U0 = hi(M1 c2) ^ c1 ^ k0
+    uint32_t r3_x3;  // r2_c3 ^ (k1 + 2 W1)
+};
+
+__host__ __device__ inline PhiloxPre philox_pre(uint32_t k0, uint32_t k1, uint32_t c1, uint32_t c2, uint32_t c3) {
+    const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
+    const uint32_t u0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t u1 = (uint32_t)p1;
+    const uint64_t p0u = (uint64_t)kPhiloxM0 * u0;
+    PhiloxPre q;
+    q.r1_x3 = c3 ^ k1;
+    q.r2_x1 = u1 ^ (k0 + kPhiloxW0);
+    q.r2_x3 = (uint32_t)(p0u >> 32) ^ (k1 + kPhiloxW1);
+    q.r2_c3 = (uint32_t)p0u;
+    q.r3_x3 = q.r2_c3 ^ (k1 + 2 * kPhiloxW1);
+    return q;
+}
+
+// Philox4x32-10 of counter (c0, c1, c2, c3) given philox_pre(k0, k1, c1, c2, c3).
+__device__ __forceinline__ U4 philox_block_pre(uint32_t k0, uint32_t k1, uint32_t c0, const PhiloxPre& q) {
+    uint64_t p0 = (uint64_t)kPhiloxM0 * c0;  // round 1
+    const uint32_t x2 = (uint32_t)(p0 >> 32) ^ q.r1_x3;
+    const uint32_t x3 = (uint32_t)p0;
+    uint64_t p1 = (uint64_t)kPhiloxM1 * x2;  // round 2
+    const uint32_t y0 = (uint32_t)(p1 >> 32) ^ q.r2_x1;
+    const uint32_t y1 = (uint32_t)p1;
+    const uint32_t y2 = x3 ^ q.r2_x3;
+    p0 = (uint64_t)kPhiloxM0 * y0;  // round 3
+    p1 = (uint64_t)kPhiloxM1 * y2;
+    U4 c{(uint32_t)(p1 >> 32) ^ y1 ^ (k0 + 2 * kPhiloxW0), (uint32_t)p1, (uint32_t)(p0 >> 32) ^ q.r3_x3,
+         (uint32_t)p0};
+    k0 += 3 * kPhiloxW0;
+    k1 += 3 * kPhiloxW1;
+#pragma unroll
+    for (int i = 3; i < 10; ++i) {
+        const uint64_t a = (uint64_t)kPhiloxM0 * c.x;
+        const uint64_t b = (uint64_t)kPhiloxM1 * c.z;
+        const uint32_t t0 = (uint32_t)(b >> 32) ^ c.y ^ k0;
+        const uint32_t t2 = (uint32_t)(a >> 32) ^ c.w ^ k1;
+        c.y = (uint32_t)b;
+        c.w = (uint32_t)a;
+        c.x = t0;
+        c.z = t2;
+        k0 += kPhiloxW0;
+        k1 += kPhiloxW1;
+    }
+    return c;
+}
+
 // 128-bit counter (lo64, hi64) + idx, carried across all four lanes
 // (_core.pyx:63-70).
 __device__ __forceinline__ U4 counter_add(uint64_t lo, uint64_t hi, uint64_t idx) {
@@ -190,17 +247,70 @@ __device__ __forceinline__ void box_muller_f64(uint32_t w0, uint32_t w1, double&
     z1 = __dmul_rn(r, s);
 }
 
-// Fast (fp32) route: u1' = (2^24 - (w0 >> 8)) * 2^-24 is exact; logf is
-// accurate to 1 ulp including near 1; 2*u2 is exact so sincospif evaluates
-// cos/sin(2 pi u2) without the fp32 rounding of 2 pi * u2.
+// Fast (fp32) route, specialised to the 24-bit inputs (DESIGN.md
+// "Tolerances"; coefficients fitted and verified exhaustively over all 2^24
+// inputs by tools/fit_boxmuller.py):
+//  * s = -2 ln u1' with u1' = m * 2^-24, m = 2^24 - (w0 >> 8) in [1, 2^24]:
+//    m -> float is exact; split m = f * 2^e with f in [sqrt(1/2), sqrt(2)),
+//    ln f = g + g^2 Q(g) (g = f - 1 exact, Q degree 7), so the relative error
+//    stays ~2 ulp even as u1' -> 1; max rel err 1.96 * 2^-24;
+//  * r = sqrt(s) as s * rsqrt(s) (MUFU.RSQ);
+//  * (cos, sin)(2 pi k / 2^24), k = w1 >> 8: the quadrant comes straight from
+//    the integer (exact argument reduction), the remainder t in [-1, 1) is
+//    exact and cos/sin(pi t / 4) are degree-8/9 polynomials; abs err
+//    1.43 * 2^-24.
+__device__ __forceinline__ float neg2_ln_u1(uint32_t w0) {
+    const float x = (float)(16777216u - (w0 >> 8));  // exact
+    const int ib = __float_as_int(x);
+    const int e = (ib - 0x3F3504F3) >> 23;
+    const float f = __int_as_float(ib - (e << 23));
+    const float g = f - 1.0f;
+    float q = 9.004202485e-02f;
+    q = fmaf(q, g, -1.425779462e-01f);
+    q = fmaf(q, g, 1.480645984e-01f);
+    q = fmaf(q, g, -1.657504737e-01f);
+    q = fmaf(q, g, 1.997310519e-01f);
+    q = fmaf(q, g, -2.500160933e-01f);
+    q = fmaf(q, g, 3.333365917e-01f);
+    q = fmaf(q, g, -4.999999404e-01f);
+    const float lnf = fmaf(g * g, q, g);
+    const float lnx = fmaf((float)(e - 24), 0.6931471805599453f, lnf);
+    return -2.0f * lnx;
+}
+
+__device__ __forceinline__ void sincos_2pi_k24(uint32_t k, float& sn, float& cs) {
+    const uint32_t kk = k + (1u << 21);
+    const uint32_t q = (kk >> 22) & 3u;
+    const float t = (float)((int)(kk & 0x3FFFFFu) - (1 << 21)) * 4.76837158203125e-07f;  // 2^-21, exact
+    const float t2 = t * t;
+    float s = 3.089971017e-07f;
+    s = fmaf(s, t2, -3.657239358e-05f);
+    s = fmaf(s, t2, 2.490393119e-03f);
+    s = fmaf(s, t2, -8.074551076e-02f);
+    s = fmaf(s, t2, 7.853981853e-01f);
+    s *= t;
+    float c = 3.529804189e-06f;
+    c = fmaf(c, t2, -3.259385994e-04f);
+    c = fmaf(c, t2, 1.585432515e-02f);
+    c = fmaf(c, t2, -3.084251285e-01f);
+    c = fmaf(c, t2, 1.0f);
+    const bool swap = q & 1u;
+    const float a = swap ? s : c;
+    const float b = swap ? c : s;
+    cs = __int_as_float(__float_as_int(a) ^ ((((q + 1u) >> 1) & 1u) << 31));
+    sn = __int_as_float(__float_as_int(b) ^ ((q >> 1) << 31));
+}
+
 __device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {
-    const float u1 = __fmul_rn((float)(16777216u - (w0 >> 8)), kUnitF);
-    const float x2 = __fmul_rn((float)(w1 >> 8), 1.1920928955078125e-07f);  // 2 * u2, exact
-    const float r = sqrtf(-2.0f * logf(u1));
-    float s, c;
-    sincospif(x2, &s, &c);
-    z0 = r * c;
-    z1 = r * s;
+    const float s2 = neg2_ln_u1(w0);
+    // s2 is 0 (u1' = 1) or >= 1.19e-7 (normal): the raw MUFU.RSQ (ftz) is safe.
+    float rs;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(s2));
+    const float r = s2 > 0.0f ? s2 * rs : 0.0f;
+    float sn, cs;
+    sincos_2pi_k24(w1 >> 8, sn, cs);
+    z0 = r * cs;
+    z1 = r * sn;
 }
 
 template <int X>

@@ -48,6 +48,7 @@ struct PhiloxBody {
     uint32_t k0, k1;
     uint32_t c0, c1, c2, c3;
     uint32_t ngroups;
+    PhiloxPre pre;  // philox_pre(k0, k1, c1, c2, c3)
     void* out;  // address of group 0
     XformParams p;
     PhiloxScalar s;  // head/tail done by this launch when s.n != 0
@@ -109,16 +110,17 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
     T* __restrict__ body = static_cast<T*>(a.out);
     if constexpr (SHIFT == 0) {
         constexpr int BPT = PhiloxBpt<T>::kValue;
-        const uint32_t nunits = (a.ngroups + BPT - 1) / BPT;
-        for (uint32_t u = gtid; u < nunits; u += gstride) {
-            const uint32_t g0 = u * BPT;
+        // Running group index and output pointer (adds on the ALU pipe; the
+        // FMA-heavy pipe is kept for the Philox multiplies).
+        const uint32_t gstep = gstride * BPT;
+        T* dst = body + (size_t)4 * BPT * gtid;
+        for (uint32_t g0 = gtid * BPT; g0 < a.ngroups; g0 += gstep, dst += (size_t)4 * gstep) {
             T o[BPT][4];
 #pragma unroll
             for (int j = 0; j < BPT; ++j) {
-                const U4 w = philox_block(a.k0, a.k1, U4{a.c0 + g0 + j, a.c1, a.c2, a.c3});
+                const U4 w = philox_block_pre(a.k0, a.k1, a.c0 + g0 + j, a.pre);
                 xform4<X>(w, a.p, o[j]);
             }
-            T* dst = body + (size_t)4 * g0;
             if (g0 + BPT <= a.ngroups) {
                 if constexpr (sizeof(T) == 4) {
 #pragma unroll
@@ -143,12 +145,14 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             const uint32_t g = tile * 31 + lane;
             // The block after a launch's last group may sit past a 2^32
             // boundary of c0: carry into the upper words (rare, predicated).
-            U4 c{a.c0 + g, a.c1, a.c2, a.c3};
-            if (c.x < a.c0) {
-                c.y += 1;
+            U4 w;
+            if (a.c0 + g >= a.c0) {
+                w = philox_block_pre(a.k0, a.k1, a.c0 + g, a.pre);
+            } else {
+                U4 c{a.c0 + g, a.c1 + 1, a.c2, a.c3};
                 if (c.y == 0 && ++c.z == 0) ++c.w;
+                w = philox_block(a.k0, a.k1, c);
             }
-            const U4 w = philox_block(a.k0, a.k1, c);
             U4 nx;
             nx.x = __shfl_down_sync(0xffffffffu, w.x, 1);
             nx.y = __shfl_down_sync(0xffffffffu, w.y, 1);
