@@ -55,13 +55,14 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
     const uint64_t t_warp0 = t - lane;
     if (t_warp0 * a.chunk >= a.n) return;  // whole warp idle (warp-uniform)
 
-    MrgState s{a.s1[0], a.s1[1], a.s1[2], a.s2[0], a.s2[1], a.s2[2]};
+    uint32_t x10 = a.s1[0], x11 = a.s1[1], x12 = a.s1[2], x20 = a.s2[0], x21 = a.s2[1], x22 = a.s2[2];
     for (uint32_t b = 0; b < a.nbits; ++b) {
         if ((t >> b) & 1) {
-            mat3_apply<kMrgC1>(&sj1[9 * b], s.x10, s.x11, s.x12);
-            mat3_apply<kMrgC2>(&sj2[9 * b], s.x20, s.x21, s.x22);
+            mat3_apply<kMrgC1>(&sj1[9 * b], x10, x11, x12);
+            mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
         }
     }
+    MrgStateMixed s{x10, x11, x12, (double)x20, (double)x21, (double)x22};
 
     T* __restrict__ out = static_cast<T*>(a.out);
     T* st = stage[warp];
@@ -70,8 +71,8 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
         if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
             for (int k = 0; k < TW; k += 2) {
-                const uint32_t w0 = mrg_step(s);
-                const uint32_t w1 = mrg_step(s);
+                const uint32_t w0 = mrg_step_mixed(s);
+                const uint32_t w1 = mrg_step_mixed(s);
                 T o0, o1;
                 xform2<X>(w0, w1, a.p, o0, o1);
                 st[lane * ROW + k] = o0;
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
             }
         } else {
 #pragma unroll
-            for (int k = 0; k < TW; ++k) st[lane * ROW + k] = xform1<X>(mrg_step(s), a.p);
+            for (int k = 0; k < TW; ++k) st[lane * ROW + k] = xform1<X>(mrg_step_mixed(s), a.p);
         }
         __syncwarp();
         if constexpr (TW == 32) {
