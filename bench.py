@@ -43,6 +43,7 @@ WORKLOADS = {
     "c2": ("mrg", "uniform", "fp64", 1 << 28, "mrg32k3a seed=777 uniform fp64 [-1,1) (C2)"),
     "c3_gauss": ("philox", "gaussian", "fp32", 1 << 30, "philox4x32x10 seed=777 gaussian fp32 (0,1) (C3)"),
     "c3_logn": ("philox", "lognormal", "fp32", 1 << 30, "philox4x32x10 seed=777 lognormal fp32 (0,1) (C3)"),
+    "c5": ("philox", "uniform", "fp32", 0, "FastCaloSim-style ~10^4 x 200k fp32 batches (C5)"),
 }
 METRIC = "Gsamples/s (and % HBM-write roofline) for Philox uniform fp32 at 1/2/4/8 B200"
 KERNEL_NAMES = {
@@ -199,6 +200,127 @@ def run_reference(args):
     return 0
 
 
+def graph_time_per_launch(torch, fn, k=20, reps=5):
+    """Device time per launch of fn() with K launches captured in one CUDA graph
+    (removes host launch overhead from small-n timings)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        fn()
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for _ in range(k):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / (k * reps)
+
+
+def run_sweep(P, torch, st, dev, world, tdist, max_log2):
+    """C4: batch-size sweep 2^10..2^max for uniform_bits u32 and uniform fp32."""
+    rows = []
+    for spec, dt, name in ((P.UniformBits(), torch.uint32, "u32"), (P.Uniform(0.0, 1.0), torch.float32, "f32")):
+        out = torch.empty(1 << max_log2, dtype=dt, device=dev)
+        for k in range(10, max_log2 + 1, 2):
+            n = 1 << k
+            ms = graph_time_per_launch(torch, lambda: P.generate(spec, st, n, out=out), k=20 if k < 28 else 4,
+                                       reps=5 if k < 28 else 2)
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            if world > 1:
+                tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            ms = float(t.item())
+            rows.append({"dist": name, "log2n_per_gpu": k, "us_per_launch": ms * 1e3,
+                         "gsamples_s": world * n / ms / 1e6, "gb_s": world * n * 4 / ms / 1e6})
+            log(f"sweep {name} 2^{k}: {ms*1e3:9.1f} us  {world*n/ms/1e6:8.1f} Gs/s")
+        del out
+        torch.cuda.empty_cache()
+    return rows
+
+
+def run_c5(args):
+    """C5: FastCaloSim-style consumer, ~10^4 single-electron events x 200k fp32 uniforms."""
+    import numpy as np
+    import torch
+
+    import paper_2109_01329_b200 as P
+    from paper_2109_01329_b200 import calosim as C
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    nev = args.events
+    ranges = [[(4000, 6500)]] * nev  # single electron: synth_params (calosim.py:156-164)
+    st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+    hits, allocs, table, final = C.plan_events(st, ranges)
+    total = sum(allocs)
+    out = torch.empty(total, dtype=torch.float32, device="cuda")
+    dtab = torch.from_numpy(table.view(np.int64).reshape(-1, 4).copy()).cuda()
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps
+
+    modes = {}
+    modes["segments_1_launch"] = timed(lambda: C.generate_segments(st, dtab, out), args.steps)
+    bg = C.BatchGraph(st, allocs, out)
+    modes["cuda_graph_per_batch"] = timed(bg.replay, args.steps)
+    modes["eager_per_batch"] = timed(lambda: C.per_batch(st, allocs, out), max(1, args.steps // 10))
+    best = min(("segments_1_launch", "cuda_graph_per_batch"), key=lambda k: modes[k])
+    value = total / modes[best] / 1e6
+
+    # e2e through the public API: plan (control draws) + one segment launch + hits back to host
+    t0 = time.perf_counter()
+    for _ in range(3):
+        h2, a2, tab2, _ = C.plan_events(st, ranges)
+        C.generate_segments(st, tab2, out)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / 3
+
+    cpu = None
+    if not args.no_cpu:
+        from oracle.cpu_baseline import CpuPath
+
+        c = CpuPath(workers=1)  # the reference runs events with the Serial backend (calosim.py:411)
+        sample = 100
+        buf = np.empty(C.DEFAULT_MIN_BATCH, dtype=np.float32)
+        t0 = time.perf_counter()
+        for e in range(sample):
+            c.burn_philox_uniform((777, 0), e * C.DEFAULT_MIN_BATCH, C.DEFAULT_MIN_BATCH, out=buf)
+        sec = (time.perf_counter() - t0) / sample
+        c.close()
+        cpu = {"value": C.DEFAULT_MIN_BATCH / sec / 1e9, "unit": "Gsamples/s", "cores": 1, "kind": c.kind,
+               "sample": f"{sample} events x 200000 fp32 uniforms, per-event generate + affine (Serial)"}
+    line = {
+        "metric": "Gsamples/s of FastCaloSim-style per-event uniform batches (C5)", "value": value,
+        "unit": "Gsamples/s", "n_gpus": 1, "steps": args.steps, "warmup": 1,
+        "ms_per_step": modes[best], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32->fp32", "data": "synthetic single-electron events (seed 777)",
+        "config": {"workload": f"{nev} events x max(3*hits,200000) fp32 uniforms at chained offsets",
+                   "samples_per_step": total, "modes_ms": modes, "best_mode": best,
+                   "events_per_s": nev / (modes[best] / 1e3)},
+        "e2e": {"value": total / e2e_s / 1e9, "unit": "Gsamples/s", "h2d_bytes_per_step": table.nbytes,
+                "d2h_bytes_per_step": 4 * nev, "includes": "plan_events (control draws) + segment launch + sync"},
+        "cpu_baseline": cpu, "gpu_launches": 1 if best == "segments_1_launch" else nev,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args):
     import torch
     import torch.distributed as tdist
@@ -304,6 +426,12 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_sample(args.cpu_n)
 
+    sweep = None
+    if args.sweep:
+        del out
+        torch.cuda.empty_cache()
+        sweep = run_sweep(P, torch, st, dev, world, tdist, args.sweep_max)
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -343,7 +471,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
+            "per_launch_ms": {"min": min(launch_ms), "median": statistics.median(launch_ms), "max": max(launch_ms)},
         }
+        if sweep is not None:
+            line["sweep"] = sweep
         print(json.dumps(line), flush=True)
     if world > 1:
         tdist.destroy_process_group()
@@ -364,11 +495,16 @@ def main():
     ap.add_argument("--ref-n", type=int, default=1 << 26)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sweep", action="store_true", help="also run the C4 batch-size sweep (CUDA-graph timed)")
+    ap.add_argument("--sweep-max", type=int, default=32)
+    ap.add_argument("--events", type=int, default=10000, help="C5 event count")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: contract requires --warmup >= 3")
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c5":
+        return run_c5(args)
     return run_ours(args)
 
 

@@ -182,6 +182,30 @@ def main():
         burns[label] = sha16(out)
     g["burn_once_sha16"] = burns
 
+    # FastCaloSim RNG consumption (calosim.simulate_event, calosim.py:269-358):
+    # per-event hits, allocations and the first uniforms of each device batch.
+    from portarng import calosim as C
+
+    geo = C.synth_geometry(2000, C.DEFAULT_REGIONS)
+    calo = {}
+    for label, scen, nev, min_batch in (("electron", C.ScenarioKind.SINGLE_ELECTRON, 40, C.DEFAULT_MIN_BATCH),
+                                        ("ttbar_small_batch", C.ScenarioKind.TTBAR, 3, 1000)):
+        params = C.synth_params(scen)
+        evs = C._synth_events(scen, nev, 777, params)
+        st = seed_engine(P, 777)
+        rows = []
+        for ev in evs:
+            pos = st.counter, st.lane_index
+            st2, res = C.simulate_event(ev, geo, params, st, min_batch=min_batch)
+            first = D.fill_uniform_unit(st, 4, "fp32")[1].values
+            rows.append({"hit_ranges": [[params[p.kind].hit_lo, params[p.kind].hit_hi] for p in ev.particles],
+                         "hits": res.hits, "allocated": res.randoms_allocated,
+                         "first4": [float(x) for x in first]})
+            st = st2
+        calo[label] = {"min_batch": min_batch, "events": rows,
+                       "final_position": int(__import__("portarng").engine.stream_position(st))}
+    g["calosim"] = calo
+
     for case in CASES:
         arrays[f"case__{case[0]}"] = run_case(case)
     g["cases"] = [list(c) for c in CASES]

@@ -1,0 +1,77 @@
+"""FastCaloSim RNG consumption (calosim.py:269-358): planning and batches.
+
+CPU part: the host bookkeeping (hits, allocations, position chain) driven by
+oracle control draws must reproduce the reference's simulate_event numbers
+(golden.json "calosim").  GPU part: plan_events, the segment kernel and the
+CUDA-graph replay reproduce the same batches as per-batch generation and the
+oracle stream.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2109_01329_b200 import calosim as C
+
+
+def _oracle_draws(key):
+    def batched(positions, counts):
+        parts = [O.words_to_unit(O.philox_words(key, p, c), "fp32").astype(np.float64)
+                 for p, c in zip(positions, counts)]
+        return np.concatenate(parts) if parts else np.zeros(0)
+
+    def one(position, count):
+        return O.words_to_unit(O.philox_words(key, position, count), "fp32").astype(np.float64)
+
+    return batched, one
+
+
+@pytest.mark.parametrize("label", ["electron", "ttbar_small_batch"])
+def test_plan_matches_reference_simulate_event(golden, label):
+    ref = golden["calosim"][label]
+    ranges = [[tuple(r) for r in e["hit_ranges"]] for e in ref["events"]]
+    hits, allocs = C.plan_from_controls(0, ranges, ref["min_batch"], *_oracle_draws(O.seed_philox(777)))
+    assert hits == [e["hits"] for e in ref["events"]]
+    assert allocs == [e["allocated"] for e in ref["events"]]
+    assert sum(allocs) == ref["final_position"]
+
+
+def test_batches_start_where_reference_batches_start(golden):
+    ref = golden["calosim"]["electron"]
+    key = O.seed_philox(777)
+    pos = 0
+    for e in ref["events"]:
+        assert O.words_to_unit(O.philox_words(key, pos, 4), "fp32").tolist() == e["first4"]
+        pos += e["allocated"]
+
+
+@pytest.mark.gpu
+def test_gpu_plan_segments_and_graph(golden):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_01329_b200 as P
+
+    for label in ("electron", "ttbar_small_batch"):
+        ref = golden["calosim"][label]
+        ranges = [[tuple(r) for r in e["hit_ranges"]] for e in ref["events"]]
+        st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+        hits, allocs, table, final = C.plan_events(st, ranges, ref["min_batch"])
+        assert hits == [e["hits"] for e in ref["events"]]
+        assert allocs == [e["allocated"] for e in ref["events"]]
+        assert P.stream_position(final) == ref["final_position"]
+        total = sum(allocs)
+        seg = torch.empty(total, dtype=torch.float32, device="cuda")
+        C.generate_segments(st, table, seg)
+        eager = torch.empty_like(seg)
+        C.per_batch(st, allocs, eager)
+        g = C.BatchGraph(st, allocs, torch.zeros_like(seg))
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(seg, eager) and torch.equal(g.out, eager)
+        want = O.words_to_unit(O.philox_words(O.seed_philox(777), 0, total), "fp32")
+        assert np.array_equal(seg.cpu().numpy(), want)
+        off = 0
+        for e in ref["events"]:
+            assert seg[off:off + 4].cpu().tolist() == e["first4"]
+            off += e["allocated"]
