@@ -339,6 +339,7 @@ int check_mrg_state(const uint32_t* s1, const uint32_t* s2) {
 struct MrgTables {
     uint32_t nbits;
     uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];
+    uint32_t h1[9], h2[9];  // A^(chunk/2)
 };
 std::mutex g_mrg_mu;
 std::map<std::pair<uint64_t, uint32_t>, MrgTables> g_mrg_tables;
@@ -351,6 +352,11 @@ const MrgTables& mrg_tables(uint64_t chunk, uint32_t nbits) {
     MrgTables t{};
     t.nbits = nbits;
     Mat3 a, b;
+    mat_pow_u64(chunk / 2, &a, &b);
+    for (int e = 0; e < 9; ++e) {
+        t.h1[e] = (uint32_t)a.v[e];
+        t.h2[e] = (uint32_t)b.v[e];
+    }
     mat_pow_u64(chunk, &a, &b);
     for (uint32_t i = 0; i < nbits; ++i) {
         for (int e = 0; e < 9; ++e) {
@@ -382,7 +388,7 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     if (rc) return rc;
     const uint64_t tmax = (uint64_t)sms * occ * kMrgThreads;
     uint64_t chunk = (n + tmax - 1) / tmax;
-    chunk = (chunk + TW - 1) / TW * TW;
+    chunk = (chunk + 2 * TW - 1) / (2 * TW) * (2 * TW);  // two interleaved halves of whole tiles
     const uint64_t tact = (n + chunk - 1) / chunk;
     uint32_t nbits = 0;
     while (nbits < 64 && ((tact - 1) >> nbits) != 0) ++nbits;
@@ -398,6 +404,8 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     a.nbits = nbits;
     memcpy(a.j1, tb.j1, sizeof a.j1);
     memcpy(a.j2, tb.j2, sizeof a.j2);
+    memcpy(a.h1, tb.h1, sizeof a.h1);
+    memcpy(a.h2, tb.h2, sizeof a.h2);
     a.out = dptr;
     a.p = p;
     const uint64_t blocks = (tact + kMrgThreads - 1) / kMrgThreads;

@@ -193,43 +193,54 @@ __global__ void __launch_bounds__(kPhiloxThreads)
                            XformParams p, typename XformTraits<X>::T* out) {
     using T = typename XformTraits<X>::T;
     static_assert(!XformTraits<X>::kPair, "segments carry single-word transforms only");
-    const uint64_t gtid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t gstride = (uint64_t)gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t gstride = gridDim.x * blockDim.x;
     for (uint32_t s = blockIdx.y; s < nseg; s += gridDim.y) {
         const PhiloxSegment sg = segs[s];
-        PhiloxScalar a;
+        PhiloxBody a;
         a.k0 = k0;
         a.k1 = k1;
+        a.p = p;
+        PhiloxScalar& sc = a.s;
+        sc.k0 = k0;
+        sc.k1 = k1;
         // block = pos >> 2 (128-bit), lane = pos & 3 (engine.py:221-222)
-        a.ctr_lo = (sg.pos_lo >> 2) | (sg.pos_hi << 62);
-        a.ctr_hi = sg.pos_hi >> 2;
-        a.lane = (uint32_t)(sg.pos_lo & 3);
-        a.n = sg.count;
+        sc.ctr_lo = (sg.pos_lo >> 2) | (sg.pos_hi << 62);
+        sc.ctr_hi = sg.pos_hi >> 2;
+        sc.lane = (uint32_t)(sg.pos_lo & 3);
+        sc.n = sg.count;
         T* dst = out + sg.out_offset;
-        // head to a 16-byte boundary, 4-element groups, tail
-        const uint64_t mis = ((16u - (uint32_t)((uintptr_t)dst & 15u)) & 15u) / sizeof(T);
-        const uint64_t i0 = mis < a.n ? mis : a.n;
-        const uint64_t ng = (a.n - i0) >> 2;
-        a.i0 = i0;
-        a.tail0 = i0 + 4 * ng;
-        const uint64_t nscalar = i0 + (a.n - a.tail0);
-        for (uint64_t q = gtid; q < nscalar; q += gstride) {
-            const uint64_t i = q < i0 ? q : a.tail0 + (q - i0);
-            dst[i] = philox_scalar<X>(a, p, i);
+        // same plan as the host launcher: scalar head to a 32-byte boundary,
+        // 4-element groups, scalar tail
+        uint64_t i0 = ((32u - (uint32_t)((uintptr_t)dst & 31u)) & 31u) / sizeof(T);
+        if (i0 > sc.n) i0 = sc.n;
+        uint64_t ng = (sc.n - i0) >> 2;
+        const uint64_t v0 = sc.lane + i0;
+        const uint64_t blk_lo = sc.ctr_lo + (v0 >> 2);
+        const uint64_t blk_hi = sc.ctr_hi + (blk_lo < sc.ctr_lo ? 1u : 0u);
+        // a segment whose blocks cross a 2^32 boundary of c0 (or is > 2^31
+        // groups) takes the all-scalar path; segments are small in practice.
+        if ((uint64_t)(uint32_t)blk_lo + ng + 1 > (1ull << 32) || ng > (1ull << 31)) {
+            i0 = sc.n;
+            ng = 0;
         }
-        const uint64_t v0 = a.lane + i0;  // virtual word of group 0
-        const uint32_t shift = (uint32_t)(v0 & 3);
-        for (uint64_t g = gtid; g < ng; g += gstride) {
-            const uint64_t v = v0 + 4 * g;
-            const U4 b0 = philox_block(k0, k1, counter_add(a.ctr_lo, a.ctr_hi, v >> 2));
-            U4 w = b0;
-            if (shift) {
-                const U4 b1 = philox_block(k0, k1, counter_add(a.ctr_lo, a.ctr_hi, (v >> 2) + 1));
-                w = shift == 1 ? funnel<1>(b0, b1) : shift == 2 ? funnel<2>(b0, b1) : funnel<3>(b0, b1);
+        sc.i0 = i0;
+        sc.tail0 = i0 + 4 * ng;
+        a.c0 = (uint32_t)blk_lo;
+        a.c1 = (uint32_t)(blk_lo >> 32);
+        a.c2 = (uint32_t)blk_hi;
+        a.c3 = (uint32_t)(blk_hi >> 32);
+        a.ngroups = (uint32_t)ng;
+        a.pre = philox_pre(k0, k1, a.c1, a.c2, a.c3);
+        a.out = dst + i0;
+        philox_scalar_range<X>(sc, p, dst, gtid, gstride);
+        if (ng) {
+            switch ((uint32_t)(v0 & 3)) {
+                case 0: philox_body<X, 0>(a, gtid, gstride); break;
+                case 1: philox_body<X, 1>(a, gtid, gstride); break;
+                case 2: philox_body<X, 2>(a, gtid, gstride); break;
+                default: philox_body<X, 3>(a, gtid, gstride); break;
             }
-            T o[4];
-            xform4<X>(w, p, o);
-            st_group(dst + i0 + 4 * g, o);
         }
     }
 }
