@@ -248,7 +248,7 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
         a.out = body;
         a.p = p;
         if (first) a.s = s;  // head/tail ride on the first launch
-        uint64_t threads = shift == 0 ? (g + PhiloxBpt<T>::kValue - 1) / PhiloxBpt<T>::kValue : (g + 30) / 31 * 32;
+        uint64_t threads = shift == 0 ? (g + PhiloxBpt<T>::kValue - 1) / PhiloxBpt<T>::kValue : (g + 125) / 126 * 32;
         const uint64_t nscalar = first ? s.i0 + (n - s.tail0) : 0;
         if (nscalar > threads) threads = nscalar;
         uint64_t blocks = (threads + kPhiloxThreads - 1) / kPhiloxThreads;

@@ -22,8 +22,8 @@
 // When (lane + i0) % 4 == 0 every group is exactly one Philox block
 // (SHIFT = 0): a thread computes BPT adjacent blocks and issues 256-bit
 // stores.  Otherwise (SHIFT = 1..3) a group straddles two blocks: lane t of a
-// warp computes block t and takes the first SHIFT words of block t+1 from lane
-// t+1 by shuffle; each warp pass emits 31 groups from 32 blocks.
+// warp computes blocks 4t..4t+3 and takes block 4t+4 from lane t+1 by
+// shuffle; each warp pass emits 126 groups from 128 blocks.
 #pragma once
 
 #include "common.cuh"
@@ -136,32 +136,55 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             }
         }
     } else {
-        // Warp-cooperative funnel: 32 blocks -> 31 groups per pass.
+        // Warp-cooperative funnel.  Lane l of a warp pass computes blocks
+        // 4l..4l+3 of the tile and takes block 4l+4 (the first block of lane
+        // l+1) by shuffle; group g = words d..3 of block g + words 0..d-1 of
+        // block g+1.  A pass covers 126 groups (the 127th needs the next
+        // tile's first block; 126 keeps every pass 32-byte aligned).
+        constexpr int BPT = 4;
+        constexpr uint32_t kTileGroups = 32 * BPT - 2;
         const uint32_t lane = threadIdx.x & 31;
         const uint32_t gwarp = gtid >> 5;
         const uint32_t nwarps = gstride >> 5;
-        const uint32_t ntiles = (uint32_t)(((uint64_t)a.ngroups + 30) / 31);
+        const uint32_t ntiles = (uint32_t)(((uint64_t)a.ngroups + kTileGroups - 1) / kTileGroups);
+        // blocks at index >= lim wrap c0 past 2^32 (only the one block after
+        // a launch's last group can be consumed there)
+        const uint64_t lim = (1ull << 32) - a.c0;
         for (uint32_t tile = gwarp; tile < ntiles; tile += nwarps) {
-            const uint32_t g = tile * 31 + lane;
-            // The block after a launch's last group may sit past a 2^32
-            // boundary of c0: carry into the upper words (rare, predicated).
-            U4 w;
-            if (a.c0 + g >= a.c0) {
-                w = philox_block_pre(a.k0, a.k1, a.c0 + g, a.pre);
+            const uint32_t gb = tile * kTileGroups + BPT * lane;
+            U4 w[BPT + 1];
+            if ((uint64_t)gb + BPT <= lim) {
+#pragma unroll
+                for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre(a.k0, a.k1, a.c0 + gb + j, a.pre);
             } else {
-                U4 c{a.c0 + g, a.c1 + 1, a.c2, a.c3};
-                if (c.y == 0 && ++c.z == 0) ++c.w;
-                w = philox_block(a.k0, a.k1, c);
+#pragma unroll
+                for (int j = 0; j < BPT; ++j) {
+                    U4 c{a.c0 + gb + j, a.c1, a.c2, a.c3};
+                    if ((uint64_t)gb + j >= lim && ++c.y == 0 && ++c.z == 0) ++c.w;
+                    w[j] = philox_block(a.k0, a.k1, c);
+                }
             }
-            U4 nx;
-            nx.x = __shfl_down_sync(0xffffffffu, w.x, 1);
-            nx.y = __shfl_down_sync(0xffffffffu, w.y, 1);
-            nx.z = __shfl_down_sync(0xffffffffu, w.z, 1);
-            nx.w = __shfl_down_sync(0xffffffffu, w.w, 1);
-            if (lane < 31 && g < a.ngroups) {
-                T o[4];
-                xform4<X>(funnel<SHIFT>(w, nx), a.p, o);
-                st_group(body + (size_t)4 * g, o);
+            w[BPT].x = __shfl_down_sync(0xffffffffu, w[0].x, 1);
+            w[BPT].y = __shfl_down_sync(0xffffffffu, w[0].y, 1);
+            w[BPT].z = __shfl_down_sync(0xffffffffu, w[0].z, 1);
+            w[BPT].w = __shfl_down_sync(0xffffffffu, w[0].w, 1);
+            T o[BPT][4];
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) xform4<X>(funnel<SHIFT>(w[j], w[j + 1]), a.p, o[j]);
+            T* dst = body + (size_t)4 * gb;
+            const uint32_t nvalid = lane == 31 ? 2 : BPT;  // groups of this lane inside the pass
+            if (nvalid == BPT && gb + BPT <= a.ngroups) {
+                if constexpr (sizeof(T) == 4) {
+                    st_group2(dst, o[0], o[1]);
+                    st_group2(dst + 8, o[2], o[3]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BPT; ++j) st_group(dst + 4 * j, o[j]);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < BPT; ++j)
+                    if (j < (int)nvalid && gb + j < a.ngroups) st_group(dst + 4 * j, o[j]);
             }
         }
     }
