@@ -149,10 +149,11 @@ UniformSpec uniform_spec_f64(double a, double b) {
     UniformSpec u{};
     const double S = b - a;
     u.p.scale_d = S * 5.9604644775390625e-08;
+    u.p.mag_d = -S * 0x1p28;  // -2^52 * scale_d
     u.p.off_d = a;
     if (S == 1.0 && a == 0.0)
         u.plan = kPlanIdentity;
-    else if (std::isinf(S) || S >= 0x1p-998)
+    else if (std::isfinite(u.p.mag_d) && S >= 0x1p-998)
         u.plan = kPlanFolded;
     else
         u.plan = kPlanTwoPass;

@@ -166,8 +166,11 @@ struct MrgStateMixed {
 };
 
 __device__ __forceinline__ uint32_t mrg_step_mixed(MrgStateMixed& s) {
-    const uint64_t t1 = (uint64_t)kMrgA12 * s.x11 + (((uint64_t)kMrgM1 << 20) - (uint64_t)kMrgA13N * s.x10);
-    const uint32_t p1 = fold_mod<kMrgC1>(t1);
+    // t < 2^53.3, so one fold leaves t' = hi*209 + lo < 2^32 + 2^29.1 < 2 m1:
+    // a single conditional subtract finishes the reduction.
+    const uint64_t t = (uint64_t)kMrgA12 * s.x11 + (((uint64_t)kMrgM1 << 20) - (uint64_t)kMrgA13N * s.x10);
+    const uint64_t t1 = (t >> 32) * kMrgC1 + (t & 0xffffffffull);
+    const uint32_t p1 = (uint32_t)(t1 >= kMrgM1 ? t1 - kMrgM1 : t1);
     constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
     double p = __dmul_rn((double)kMrgA21, s.y22);
     p = __fma_rn(-(double)kMrgA23N, s.y20, p);
@@ -197,7 +200,11 @@ __device__ __forceinline__ void mat3_apply(const uint32_t* J, uint32_t& a, uint3
 // ---------------------------------------------------------- transforms
 // Word -> unit: (w >> 8) * 2^-24, exact in fp32 and fp64 (distributions.py:78-87).
 __device__ __forceinline__ float unit_f32(uint32_t w) { return __fmul_rn((float)(w >> 8), kUnitF); }
-__device__ __forceinline__ double unit_f64(uint32_t w) { return __dmul_rn((double)(w >> 8), kUnitD); }
+// 2^52 + (w >> 8) built from bits (no I2F.F64 on the XU pipe): the 24-bit
+// integer sits in the low mantissa bits of 2^52.
+__device__ __forceinline__ double u24_magic(uint32_t w) { return __hiloint2double(0x43300000, (int)(w >> 8)); }
+// (2^52 + x) * 2^-24 - 2^28 = x * 2^-24 exactly (one DFMA).
+__device__ __forceinline__ double unit_f64(uint32_t w) { return __fma_rn(u24_magic(w), kUnitD, -268435456.0); }
 
 // Parameters of one fused request.  For uniform: (a, b) -> scale/offset with
 // the reference's precision rules (distributions.py:98-104 under numpy
@@ -205,6 +212,7 @@ __device__ __forceinline__ double unit_f64(uint32_t w) { return __dmul_rn((doubl
 struct XformParams {
     float scale_f, off_f;    // uniform fp32: f32(b - a) * 2^-24, f32(a); gaussian fp32: stddev, mean
     double scale_d, off_d;   // uniform fp64: (b - a) * 2^-24, a; gaussian fp64: stddev, mean
+    double mag_d;            // uniform fp64: -2^52 * scale_d
     double ln_scale, ln_displ;  // lognormal: scale, displ (fp64 path) ...
     float ln_scale_f, ln_displ_f;  // ... and fp32 path
 };
@@ -254,25 +262,101 @@ template <> __device__ __forceinline__ float xform1<kUniformF32>(uint32_t w, con
     return __fadd_rn(__fmul_rn((float)(w >> 8), p.scale_f), p.off_f);
 }
 
+// fl(x * S') as fma(2^52 + x, S', -2^52 S'): the FMA's exact intermediate is
+// x * S', rounded once (the host keeps 2^52 S' finite, api.cu).
 template <> __device__ __forceinline__ double xform1<kUniformF64>(uint32_t w, const XformParams& p) {
-    return __dadd_rn(__dmul_rn((double)(w >> 8), p.scale_d), p.off_d);
+    return __dadd_rn(__fma_rn(u24_magic(w), p.scale_d, p.mag_d), p.off_d);
 }
 
 // Box-Muller on one word pair (distributions.py:107-131, _core.pyx:116-121):
 // u1' = 1 - u1 in (0, 1], r = sqrt(-2 ln u1'), t = 2 pi u2, (r cos t, r sin t).
 //
-// Accurate (fp64) route: the reference's own formula in double precision with
-// CUDA's libdevice log / sincos (<= 1 / 2 ulp), then `z*stddev + mean` as two
-// roundings (distributions.py:129-130).
+// Accurate (fp64) route, specialised to the 24-bit inputs (the general
+// libdevice log/sincos cost ~3x more; the reference's own libm formula is the
+// oracle):
+//  * -2 ln u1' with u1' = m 2^-24: m = f 2^e, f in [sqrt(1/2), sqrt(2)),
+//    ln f = 2 atanh(s), s = (f-1)/(f+1), |s| <= 0.1716, series to s^19
+//    (truncation < 2^-56); g = f - 1 is exact so the relative accuracy holds
+//    as u1' -> 1; e ln2 with a split constant;
+//  * r = sqrt(.) (IEEE);
+//  * cos/sin(2 pi k 2^-24), k = w1 >> 8: exact integer quadrant reduction,
+//    t in [-1, 1) exact, Taylor polynomials of pi t / 4 to t^17 / t^18
+//    (truncation < 1e-19).  The reference evaluates cos(fl(2 pi u2)); the
+//    argument rounding it carries (<= 2^-51 absolute) is inside the stated
+//    tolerance.
+// fp64 coefficients live in the constant bank: DFMA takes c[][] operands
+// directly, whereas 64-bit literals cost two UMOVs per use inside the loop.
+__constant__ double kAtanhC[9] = {0.3333333333333333,  0.2,  0.14285714285714285, 0.1111111111111111,
+                                  0.09090909090909091, 0.07692307692307693, 0.06666666666666667,
+                                  0.058823529411764705, 0.05263157894736842};  // 1/(2k+1), k = 1..9
+__constant__ double kLn2Split[2] = {0.6931467056274414, 4.7493250390316726e-07};
+__constant__ double kSinC[9] = {0.7853981633974483,     -0.08074551218828079,   0.0024903945701927202,
+                                -3.657620418217725e-05, 3.1336168903781217e-07, -1.757247673443401e-09,
+                                6.948453273886629e-12,  -2.0410263396641442e-14, 4.628704628834683e-17};
+__constant__ double kCosC[10] = {1.0,                    -0.30842513753404244,   0.015854344243815502,
+                                 -0.00032599188692739,   3.59086044859151e-06,   -2.4611369504942e-08,
+                                 1.1501159127974052e-10, -3.8980731712596753e-13, 1.001886461636272e-15,
+                                 -2.019653396886682e-18};
+
+__device__ __forceinline__ double neg2_ln_u1_f64(uint32_t w0) {
+    const double x = (double)(16777216u - (w0 >> 8));  // exact, in [1, 2^24]
+    const int hi = __double2hiint(x);
+    const int e = (hi - 0x3FE6A09E) >> 20;  // 0x3FE6A09E: high word of sqrt(1/2)
+    const double f = __hiloint2double(hi - (e << 20), __double2loint(x));
+    const double g = f - 1.0;  // exact
+    const double d = f + 1.0;
+    double rd;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(d));
+    double er = __fma_rn(-d, rd, 1.0);
+    rd = __fma_rn(rd, er, rd);
+    er = __fma_rn(-d, rd, 1.0);
+    rd = __fma_rn(rd, er, rd);
+    const double s = g * rd;
+    const double z = s * s;
+    double p = kAtanhC[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) p = __fma_rn(p, z, kAtanhC[i]);
+    const double lnf = __fma_rn(2.0 * s, z * p, 2.0 * s);
+    const double ee = (double)(e - 24);
+    const double lnx = __fma_rn(ee, kLn2Split[0], __fma_rn(ee, kLn2Split[1], lnf));
+    return -2.0 * lnx;
+}
+
+__device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, double& cs) {
+    const uint32_t kk = k + (1u << 21);
+    const uint32_t q = (kk >> 22) & 3u;
+    const double t = (double)((int)(kk & 0x3FFFFFu) - (1 << 21)) * 4.76837158203125e-07;  // exact
+    const double t2 = t * t;
+    double s = kSinC[8];
+#pragma unroll
+    for (int i = 7; i >= 0; --i) s = __fma_rn(s, t2, kSinC[i]);
+    s = s * t;
+    double c = kCosC[9];
+#pragma unroll
+    for (int i = 8; i >= 0; --i) c = __fma_rn(c, t2, kCosC[i]);
+    const bool swap = q & 1u;
+    const double a = swap ? s : c;
+    const double b = swap ? c : s;
+    cs = (((q + 1u) >> 1) & 1u) ? -a : a;
+    sn = (q >> 1) ? -b : b;
+}
+
 __device__ __forceinline__ void box_muller_f64(uint32_t w0, uint32_t w1, double& z0, double& z1) {
-    const double u1 = 1.0 - unit_f64(w0);
-    const double u2 = unit_f64(w1);
-    const double r = sqrt(__dmul_rn(-2.0, log(u1)));
-    const double t = __dmul_rn(kTwoPi, u2);
+    const double r = sqrt(neg2_ln_u1_f64(w0));
     double s, c;
-    sincos(t, &s, &c);
-    z0 = __dmul_rn(r, c);
-    z1 = __dmul_rn(r, s);
+    sincos_2pi_k24_f64(w1 >> 8, s, c);
+    // The reference takes cos/sin of fl(TWO_PI * u2) (distributions.py:125,
+    // _core.pyx:119), i.e. of 2 pi u2 + delta with
+    // delta = fl(TWO_PI u2) - TWO_PI u2 - (2 pi - TWO_PI) u2, |delta| < 1e-15.
+    // First-order correction reproduces that argument (and the reference's
+    // non-zero values at the exact quadrant points, e.g. cos(fl(pi/2))).
+    const double u2 = unit_f64(w1);
+    const double t = __dmul_rn(kTwoPi, u2);
+    const double delta = __fma_rn(-2.4492935982947064e-16, u2, -__fma_rn(kTwoPi, u2, -t));
+    const double c2 = __fma_rn(-delta, s, c);
+    const double s2 = __fma_rn(delta, c, s);
+    z0 = __dmul_rn(r, c2);
+    z1 = __dmul_rn(r, s2);
 }
 
 // Fast (fp32) route, specialised to the 24-bit inputs (DESIGN.md

@@ -9,10 +9,9 @@
 // one 3x3 mod-m mat-vec per set bit of t.  The chunk is run as two halves
 // (second start = A^(chunk/2) x first start) whose recurrences are
 // interleaved step by step, so every thread carries two independent
-// dependency chains.  Each TILE-word tile of both halves is transposed
-// through shared memory so the warp stores whole 128-byte lines: store step
-// j writes element `lane` of run j (4-byte outputs) or element lane&15 of
-// run 2j+(lane>>4) (8-byte outputs), with a running pointer per lane.
+// dependency chains.  Each 128-byte tile of both halves is transposed
+// through an XOR-swizzled shared-memory stage (16-byte chunks) so the warp
+// writes four runs' whole 128-byte lines per 128-bit store instruction.
 #pragma once
 
 #include "common.cuh"
@@ -34,29 +33,58 @@ struct MrgLaunch {
     XformParams p;
 };
 
-template <typename T> struct MrgTile { static constexpr int kWords = 32, kPad = 1; };
-template <> struct MrgTile<double> { static constexpr int kWords = 16, kPad = 1; };
+template <typename T> struct MrgTile { static constexpr int kWords = 32; };
+template <> struct MrgTile<double> { static constexpr int kWords = 16; };
 
-// Write one staged tile (32 runs of TW elements, run j = lane j's tile) to
-// out: run j starts at run0 + j*chunk.
-template <typename T, int TW, int ROW>
-__device__ __forceinline__ void mrg_store_tile(const T* st, T* __restrict__ run0, uint64_t chunk, uint32_t lane,
-                                               uint64_t first_elem, uint64_t n) {
-    const bool full = first_elem + 31 * chunk + TW <= n;  // warp-uniform
-    if constexpr (TW == 32) {
-        T* p = run0 + lane;
-        uint64_t e = first_elem + lane;
-#pragma unroll 4
-        for (int j = 0; j < 32; ++j, p += chunk, e += chunk)
-            if (full || e < n) *p = st[j * ROW + lane];
+// Shared-memory stage of one warp: 32 rows (one per lane's run) of 8
+// 16-byte chunks, chunk c of row r stored at physical chunk c ^ (r & 7)
+// (XOR swizzle: the per-lane 128-bit writes and the row-wise 128-bit reads
+// are both bank-conflict free within each 8-lane phase).
+template <typename T>
+__device__ __forceinline__ uint4 pack16(const T* v) {
+    if constexpr (sizeof(T) == 4) {
+        const uint32_t* u = reinterpret_cast<const uint32_t*>(v);
+        return make_uint4(u[0], u[1], u[2], u[3]);
     } else {
-        const uint32_t x = lane & 15;
-        const uint32_t r = lane >> 4;
-        T* p = run0 + r * chunk + x;
-        uint64_t e = first_elem + r * chunk + x;
-#pragma unroll 4
-        for (int j2 = 0; j2 < 16; ++j2, p += 2 * chunk, e += 2 * chunk)
-            if (full || e < n) *p = st[(2 * j2 + r) * ROW + x];
+        return make_uint4((uint32_t)__double2loint(v[0]), (uint32_t)__double2hiint(v[0]),
+                          (uint32_t)__double2loint(v[1]), (uint32_t)__double2hiint(v[1]));
+    }
+}
+
+__device__ __forceinline__ void stage_put(uint4* st, uint32_t lane, int c, uint4 v) {
+    st[lane * 8 + (c ^ (lane & 7))] = v;
+}
+
+__device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Write one staged tile (row j = run j, starting at run0 + j*chunk).  Each
+// instruction moves four runs' 128-byte lines: lane L handles row
+// 4i + (L >> 3), chunk L & 7.
+template <typename T>
+__device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ run0, uint64_t chunk, uint32_t lane,
+                                               uint64_t first_elem, uint64_t n, bool vec_ok) {
+    constexpr int CE = 16 / sizeof(T);
+    constexpr int TW = 8 * CE;
+    const bool full = vec_ok && first_elem + 31 * chunk + TW <= n;  // warp-uniform
+    const uint32_t x = lane & 7;
+    const uint32_t r0 = lane >> 3;
+    T* p = run0 + r0 * chunk + x * CE;
+    uint64_t e = first_elem + r0 * chunk + x * CE;
+#pragma unroll 2
+    for (int i = 0; i < 8; ++i, p += 4 * chunk, e += 4 * chunk) {
+        const uint32_t j = 4 * i + r0;
+        const uint4 v = st[j * 8 + (x ^ (j & 7))];
+        if (full) {
+            st_global_cs_v4(p, v);
+        } else {
+            const T* vv = reinterpret_cast<const T*>(&v);
+#pragma unroll
+            for (int q = 0; q < CE; ++q)
+                if (e + q < n) p[q] = vv[q];
+        }
     }
 }
 
@@ -64,9 +92,8 @@ template <int X>
 __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
     using T = typename XformTraits<X>::T;
     constexpr int TW = MrgTile<T>::kWords;
-    constexpr int ROW = TW + MrgTile<T>::kPad;
     constexpr int WARPS = kMrgThreads / 32;
-    __shared__ T stage[2][WARPS][32 * ROW];
+    __shared__ uint4 stage[2][WARPS][32 * 8];
     __shared__ uint32_t sj1[kMrgMaxBits * 9], sj2[kMrgMaxBits * 9];
 
     for (uint32_t i = threadIdx.x; i < a.nbits * 9; i += blockDim.x) {
@@ -95,39 +122,41 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
 
     const uint64_t half = a.chunk >> 1;
     T* __restrict__ out = static_cast<T*>(a.out);
-    T* sta = stage[0][warp];
-    T* stb = stage[1][warp];
+    uint4* sta = stage[0][warp];
+    uint4* stb = stage[1][warp];
+    const bool vec_ok = ((uintptr_t)out & 15u) == 0;
     const uint64_t warp_elem0 = t_warp0 * a.chunk;
+    constexpr int CE = 16 / sizeof(T);  // elements per 16-byte chunk
     for (uint64_t off = 0; off < half; off += TW) {
         if (warp_elem0 + off >= a.n) break;  // warp-uniform
-        if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
-            for (int k = 0; k < TW; k += 2) {
-                const uint32_t a0 = mrg_step_mixed(sa);
-                const uint32_t b0 = mrg_step_mixed(sb);
-                const uint32_t a1 = mrg_step_mixed(sa);
-                const uint32_t b1 = mrg_step_mixed(sb);
-                T o0, o1;
-                xform2<X>(a0, a1, a.p, o0, o1);
-                sta[lane * ROW + k] = o0;
-                sta[lane * ROW + k + 1] = o1;
-                xform2<X>(b0, b1, a.p, o0, o1);
-                stb[lane * ROW + k] = o0;
-                stb[lane * ROW + k + 1] = o1;
-            }
-        } else {
+        for (int c = 0; c < 8; ++c) {
+            T oa[CE], ob[CE];
+            if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
-            for (int k = 0; k < TW; ++k) {
-                const uint32_t wa = mrg_step_mixed(sa);
-                const uint32_t wb = mrg_step_mixed(sb);
-                sta[lane * ROW + k] = xform1<X>(wa, a.p);
-                stb[lane * ROW + k] = xform1<X>(wb, a.p);
+                for (int k = 0; k < CE; k += 2) {
+                    const uint32_t a0 = mrg_step_mixed(sa);
+                    const uint32_t b0 = mrg_step_mixed(sb);
+                    const uint32_t a1 = mrg_step_mixed(sa);
+                    const uint32_t b1 = mrg_step_mixed(sb);
+                    xform2<X>(a0, a1, a.p, oa[k], oa[k + 1]);
+                    xform2<X>(b0, b1, a.p, ob[k], ob[k + 1]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < CE; ++k) {
+                    const uint32_t wa = mrg_step_mixed(sa);
+                    const uint32_t wb = mrg_step_mixed(sb);
+                    oa[k] = xform1<X>(wa, a.p);
+                    ob[k] = xform1<X>(wb, a.p);
+                }
             }
+            stage_put(sta, lane, c, pack16<T>(oa));
+            stage_put(stb, lane, c, pack16<T>(ob));
         }
         __syncwarp();
-        mrg_store_tile<T, TW, ROW>(sta, out + warp_elem0 + off, a.chunk, lane, warp_elem0 + off, a.n);
-        mrg_store_tile<T, TW, ROW>(stb, out + warp_elem0 + half + off, a.chunk, lane, warp_elem0 + half + off,
-                                   a.n);
+        mrg_store_tile<T>(sta, out + warp_elem0 + off, a.chunk, lane, warp_elem0 + off, a.n, vec_ok);
+        mrg_store_tile<T>(stb, out + warp_elem0 + half + off, a.chunk, lane, warp_elem0 + half + off, a.n, vec_ok);
         __syncwarp();
     }
 }

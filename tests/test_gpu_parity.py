@@ -370,3 +370,23 @@ def test_state_round_trip_matches_reference_accounting():
         s, w = P.next_word(s)
         words.append(w)
     assert tuple(words) == (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)
+
+
+@pytest.mark.parametrize("prec,method", [("fp64", "accurate"), ("fp32", "fast"), ("fp32", "accurate")])
+def test_box_muller_exhaustive_24bit(prec, method):
+    """Every one of the 2^24 possible u1 (and, separately, u2) values through
+    gaussian_from_words vs the oracle's libm Box-Muller: the stated tolerance
+    holds over the whole input domain, not just sampled streams."""
+    k = np.arange(1 << 24, dtype=np.uint64)
+    other = ((k * 2654435761) & 0xFFFFFF).astype(np.uint32)
+    kk = k.astype(np.uint32)
+    for first, second in ((kk, other), (other, kk)):
+        words = np.empty(2 << 24, dtype=np.uint32)
+        words[0::2] = first << np.uint32(8)
+        words[1::2] = second << np.uint32(8)
+        want = O.gaussian_from_words(words, 0.0, 1.0, 2 << 24, prec)
+        got = host(P.gaussian_from_words(torch.from_numpy(words).cuda(), 0.0, 1.0, 2 << 24, prec, method))
+        dt = np.float32 if prec == "fp32" else np.float64
+        err, exact = check_close(got, want, gaussian_allowed(want, 0.0, 1.0, dt, method == "fast"),
+                                 f"{prec}/{method}")
+        print(f"{prec}/{method}: max abs err {err:.3e}, bit-exact fraction {exact:.6f}")
