@@ -15,6 +15,15 @@ for p in (str(REPO), str(REPO / "tests")):
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running test")
+    # Build the CUDA library (nvcc cross-compiles without a GPU) and the CPU
+    # checker if a fresh checkout lacks them; the package itself never falls
+    # back to anything else.
+    import subprocess
+
+    if not (REPO / "paper_2109_01329_b200" / "libprng_b200.so").exists():
+        subprocess.run(["make", "-s", "-C", str(REPO / "paper_2109_01329_b200" / "csrc")], check=True)
+    if not (REPO / "oracle" / "liboracle.so").exists():
+        subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
 
 
 @pytest.fixture(scope="session")
