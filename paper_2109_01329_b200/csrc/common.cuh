@@ -134,27 +134,11 @@ __device__ __forceinline__ uint32_t fold_mod(uint64_t t) {
     return (uint32_t)(t >= M ? t - M : t);
 }
 
-// One MRG32k3a step of both components (_core.pyx:85-101).  Signed products
-// are offset by a multiple of the modulus to stay in unsigned 64-bit:
-// a12*x11 - a13n*x10 + 2^20*m1 is in [0, 2^53.3); a21*x22 - a23n*x20 + 2^21*m2
-// in [0, 2^53.4).  Returns z = (p1 - p2) mod m1.
-struct MrgState {
-    uint32_t x10, x11, x12, x20, x21, x22;
-};
-
-__device__ __forceinline__ uint32_t mrg_step(MrgState& s) {
-    const uint64_t t1 = (uint64_t)kMrgA12 * s.x11 + (((uint64_t)kMrgM1 << 20) - (uint64_t)kMrgA13N * s.x10);
-    const uint64_t t2 = (uint64_t)kMrgA21 * s.x22 + (((uint64_t)kMrgM2 << 21) - (uint64_t)kMrgA23N * s.x20);
-    const uint32_t p1 = fold_mod<kMrgC1>(t1);
-    const uint32_t p2 = fold_mod<kMrgC2>(t2);
-    s.x10 = s.x11; s.x11 = s.x12; s.x12 = p1;
-    s.x20 = s.x21; s.x21 = s.x22; s.x22 = p2;
-    return p1 >= p2 ? p1 - p2 : p1 - p2 + kMrgM1;
-}
-
-// Mixed-pipe MRG32k3a step: component 1 in 64-bit integer arithmetic (the
-// FMA-heavy pipe's IMAD.WIDE), component 2 in exact fp64 arithmetic on the
-// FP64 pipe (L'Ecuyer's floating-point formulation), so the two halves of a
+// One MRG32k3a step (_core.pyx:85-101), returning z = (p1 - p2) mod m1.
+// Mixed-pipe formulation: component 1 in 64-bit integer arithmetic on the
+// FMA-heavy pipe's IMAD.WIDE (signed products offset by 2^20*m1 to stay
+// unsigned: a12*x11 - a13n*x10 + 2^20*m1 is in [0, 2^53.3)), component 2 in
+// exact fp64 arithmetic on the FP64 pipe (L'Ecuyer's floating-point formulation), so the two halves of a
 // step run on different execution units.  All fp64 values are integers
 // below 2^53, every operation is exact:
 //   p = a21*x22 - a23n*x20          (|p| < 2^52.4: DMUL + DFMA, exact)

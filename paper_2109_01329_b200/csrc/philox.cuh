@@ -112,27 +112,31 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
         constexpr int BPT = PhiloxBpt<T>::kValue;
         // Running group index and output pointer (adds on the ALU pipe; the
         // FMA-heavy pipe is kept for the Philox multiplies).
+        // The steady-state loop covers whole units only (no per-iteration
+        // bounds branch); the < BPT leftover groups go to one thread after it.
         const uint32_t gstep = gstride * BPT;
+        const uint32_t gfull = a.ngroups - a.ngroups % BPT;
         T* dst = body + (size_t)4 * BPT * gtid;
-        for (uint32_t g0 = gtid * BPT; g0 < a.ngroups; g0 += gstep, dst += (size_t)4 * gstep) {
+        for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
             T o[BPT][4];
 #pragma unroll
             for (int j = 0; j < BPT; ++j) {
                 const U4 w = philox_block_pre(a.k0, a.k1, a.c0 + g0 + j, a.pre);
                 xform4<X>(w, a.p, o[j]);
             }
-            if (g0 + BPT <= a.ngroups) {
-                if constexpr (sizeof(T) == 4) {
+            if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                    for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < BPT; ++j) st_group(dst + 4 * j, o[j]);
-                }
+                for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
             } else {
 #pragma unroll
-                for (int j = 0; j < BPT; ++j)
-                    if (g0 + j < a.ngroups) st_group(dst + 4 * j, o[j]);
+                for (int j = 0; j < BPT; ++j) st_group(dst + 4 * j, o[j]);
+            }
+        }
+        if (gtid == gstride - 1) {
+            for (uint32_t g = gfull; g < a.ngroups; ++g) {
+                T o[4];
+                xform4<X>(philox_block_pre(a.k0, a.k1, a.c0 + g, a.pre), a.p, o);
+                st_group(body + (size_t)4 * g, o);
             }
         }
     } else {
