@@ -390,3 +390,64 @@ def test_box_muller_exhaustive_24bit(prec, method):
         err, exact = check_close(got, want, gaussian_allowed(want, 0.0, 1.0, dt, method == "fast"),
                                  f"{prec}/{method}")
         print(f"{prec}/{method}: max abs err {err:.3e}, bit-exact fraction {exact:.6f}")
+
+
+@pytest.mark.parametrize("strategy", ["pipelined", "zero_copy"])
+def test_host_generation_matches_device(strategy):
+    from paper_2109_01329_b200.hostpath import HostGenerator
+
+    st = P.skip_ahead(P.seed_engine(PHILOX, 777), 12345)
+    for spec, n in ((P.Uniform(-2.0, 3.0), (1 << 25) + 3), (P.Gaussian(1.0, 2.0, "fp64"), 100001),
+                    (P.UniformBits(), 77)):
+        hg = HostGenerator(chunk=1 << 22, strategy=strategy)
+        host_buf = torch.empty(n, dtype=P.distributions.out_dtype(spec), pin_memory=True)
+        new = hg.generate(spec, st, n, host_buf)
+        hg.synchronize()
+        new2, dev = P.generate(spec, st, n)
+        assert new == new2
+        assert torch.equal(host_buf, dev.cpu())
+
+
+def test_lognormal_parameters_and_mrg_pairs():
+    st = P.skip_ahead(P.seed_engine(MRG, 31337), 5)
+    s1, s2 = O.mrg_skip(*O.seed_mrg(31337), 5)
+    for prec in ("fp32", "fp64"):
+        for n in (1, 2, 999, 4097):
+            want = O.generate("mrg", (s1, s2), "lognormal", n, prec, 0.3, 0.7, displ=-1.5, scale=2.5)
+            _, got = P.generate(P.Lognormal(0.3, 0.7, -1.5, 2.5, prec, "accurate"), st, n)
+            dt = np.float32 if prec == "fp32" else np.float64
+            # x = displ + scale * exp(g): tolerance on the exp part, then shifted
+            allowed = lognormal_allowed((want - (-1.5)) / 2.5, 0.3, 0.7, dt, False) * 2.5 + 4 * np.spacing(
+                np.abs(want).astype(dt)).astype(np.float64)
+            check_close(host(got), want, allowed, f"logn {prec} n={n}")
+            wg = O.generate("mrg", (s1, s2), "gaussian", n, prec, -4.0, 0.25)
+            _, gg = P.generate(P.Gaussian(-4.0, 0.25, prec, "accurate"), st, n)
+            check_close(host(gg), wg, gaussian_allowed(wg, -4.0, 0.25, dt, False), f"mrg gauss {prec} n={n}")
+
+
+def test_uniform_degenerate_scales_follow_numpy_semantics():
+    """Ranges whose scale underflows the folded form (two-pass plan) or
+    overflows to inf (numpy gives nan at u=0, inf elsewhere) match the oracle."""
+    st = P.seed_engine(PHILOX, 5)
+    key = O.seed_philox(5)
+    cases = [(0.0, 2.0 ** -110, "fp32"), (0.0, 2.0 ** -1000, "fp64"), (-3e38, 3e38, "fp32"),
+             (-1e308, 1e308, "fp64")]
+    for lo, hi, prec in cases:
+        want = O.range_transform(O.words_to_unit(O.philox_words(key, 0, 5000), prec), lo, hi)
+        _, got = P.generate(P.Uniform(lo, hi, prec), st, 5000)
+        assert np.array_equal(host(got), want, equal_nan=True), (lo, hi, prec)
+
+
+def test_bad_output_buffers_are_rejected():
+    st = P.seed_engine(PHILOX, 5)
+    buf = torch.empty(100, dtype=torch.float32, device="cuda")
+    misaligned = buf.data_ptr() + 4  # only 4-byte aligned: invalid for fp64 output
+    from paper_2109_01329_b200 import _lib
+
+    k0, k1, ctr, lane = P.engine.philox_args(st)
+    rc = _lib.lib.prng_philox4x32x10_uniform_f64(k0, k1, ctr, lane, 10, 0.0, 1.0, misaligned, None)
+    assert rc == _lib.PRNG_ERR_INVALID_PARAMETER
+    pageable = np.zeros(16, dtype=np.uint32)
+    rc = _lib.lib.prng_philox4x32x10_bits(k0, k1, ctr, lane, 16, pageable.ctypes.data, None)
+    assert rc in (_lib.PRNG_ERR_INVALID_PARAMETER, _lib.PRNG_ERR_CUDA)
+    assert _lib.lib.prng_last_error()
