@@ -26,7 +26,9 @@ from .distributions import (
 )
 from .engine import (
     EngineKind,
+    Mrg32k3a,
     Mrg32k3aState,
+    Philox4x32x10,
     PhiloxState,
     generate_words,
     mrg_unit,
@@ -47,7 +49,9 @@ __all__ = [
     "InvalidParameter",
     "InvalidRange",
     "Lognormal",
+    "Mrg32k3a",
     "Mrg32k3aState",
+    "Philox4x32x10",
     "PhiloxState",
     "RandomBlock",
     "Uniform",

@@ -27,8 +27,11 @@ from typing import Tuple, Union
 
 from . import _lib
 from .engine import (
+    EngineKind,
     EngineState,
+    Mrg32k3a,
     Mrg32k3aState,
+    Philox4x32x10,
     PhiloxState,
     _out_tensor,
     _stream_handle,
@@ -167,37 +170,46 @@ def gaussian_from_words(words, mean: float, stddev: float, n: int, precision: st
     return out[:n]
 
 
-def _launch(spec: DistributionSpec, state: EngineState, n: int, ptr: int, s) -> None:
-    L = _lib.lib
-    if isinstance(state, PhiloxState):
-        k0, k1, ctr, lane = philox_args(state)
-        head = (k0, k1, ctr, lane, n)
-        prefix = "prng_philox4x32x10_"
-    elif isinstance(state, Mrg32k3aState):
-        s1, s2 = mrg_args(state)
-        head = (s1, s2, n)
-        prefix = "prng_mrg32k3a_"
-    else:
-        raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+_PREFIX = {EngineKind.PHILOX4X32X10: "prng_philox4x32x10_", EngineKind.MRG32K3A: "prng_mrg32k3a_"}
+_FN_CACHE = {}
+
+
+def _entry(kind: EngineKind, spec: DistributionSpec):
+    """The C-ABI function and the distribution arguments for one request shape."""
     if isinstance(spec, UniformBits):
-        rc = getattr(L, prefix + "bits")(*head, ptr, s)
+        name, tail = "bits", ()
     elif isinstance(spec, Uniform):
-        rc = getattr(L, prefix + "uniform_" + ("f32" if spec.precision == "fp32" else "f64"))(
-            *head, spec.lo, spec.hi, ptr, s)
+        name, tail = "uniform_" + ("f32" if spec.precision == "fp32" else "f64"), (spec.lo, spec.hi)
     elif isinstance(spec, Gaussian):
         if spec.precision == "fp32":
-            rc = getattr(L, prefix + "gaussian_f32")(*head, spec.mean, spec.stddev, _METHODS[spec.method], ptr, s)
+            name, tail = "gaussian_f32", (spec.mean, spec.stddev, _METHODS[spec.method])
         else:
-            rc = getattr(L, prefix + "gaussian_f64")(*head, spec.mean, spec.stddev, ptr, s)
+            name, tail = "gaussian_f64", (spec.mean, spec.stddev)
     elif isinstance(spec, Lognormal):
         if spec.precision == "fp32":
-            rc = getattr(L, prefix + "lognormal_f32")(*head, spec.m, spec.s, spec.displ, spec.scale,
-                                                       _METHODS[spec.method], ptr, s)
+            name, tail = "lognormal_f32", (spec.m, spec.s, spec.displ, spec.scale, _METHODS[spec.method])
         else:
-            rc = getattr(L, prefix + "lognormal_f64")(*head, spec.m, spec.s, spec.displ, spec.scale, ptr, s)
+            name, tail = "lognormal_f64", (spec.m, spec.s, spec.displ, spec.scale)
     else:
         raise InvalidParameter(f"unknown distribution {spec!r}")
-    _lib.check(rc)
+    key = (kind, name)
+    fn = _FN_CACHE.get(key)
+    if fn is None:
+        fn = _FN_CACHE[key] = getattr(_lib.lib, _PREFIX[kind] + name)
+    return fn, tail
+
+
+def _launch(spec: DistributionSpec, state, n: int, ptr: int, s) -> None:
+    if isinstance(state, (Philox4x32x10, Mrg32k3a)):
+        kind, head = state.kind, state.launch_args()
+    elif isinstance(state, PhiloxState):
+        kind, head = EngineKind.PHILOX4X32X10, philox_args(state)
+    elif isinstance(state, Mrg32k3aState):
+        kind, head = EngineKind.MRG32K3A, mrg_args(state)
+    else:
+        raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
+    fn, tail = _entry(kind, spec)
+    _lib.check(fn(*head, n, *tail, ptr, s))
 
 
 def out_dtype(spec: DistributionSpec):
@@ -216,7 +228,10 @@ def generate(distribution: DistributionSpec, engine: EngineState, n: int, out=No
     out = _out_tensor(out, n, out_dtype(distribution))
     if n:
         _launch(distribution, engine, n, out.data_ptr(), _stream_handle(stream, out.device))
-    new_state = advance(engine, words_consumed(distribution, n))
+    if isinstance(engine, (Philox4x32x10, Mrg32k3a)):
+        new_state = engine.skip_ahead(words_consumed(distribution, n))  # oneMKL engines advance in place
+    else:
+        new_state = advance(engine, words_consumed(distribution, n))
     return new_state, (out if out.numel() == n else out[:n])
 
 

@@ -237,3 +237,90 @@ def next_word(state: EngineState):
 def mrg_unit(z: int) -> float:
     """engine.py:178-180."""
     return z / (MRG_M1 + 1)
+
+
+class Philox4x32x10:
+    """oneMKL-style stateful engine (`oneapi::mkl::rng::philox4x32x10(queue,
+    seed)`, the interface the paper extends).
+
+    Holds the key and the absolute word position; `generate(distr, engine,
+    n, out)` advances it in place.  `state` / `from_state` convert to and
+    from the reference's immutable PhiloxState (engine.py:57-72).
+    """
+
+    kind = EngineKind.PHILOX4X32X10
+
+    def __init__(self, seed: int = 0, offset: int = 0):
+        st = seed_engine(EngineKind.PHILOX4X32X10, seed)
+        self.key = st.key
+        self.position = 0
+        self._ctr = (ctypes.c_uint32 * 4)()
+        if offset:
+            self.skip_ahead(offset)
+
+    @classmethod
+    def from_state(cls, state: PhiloxState) -> "Philox4x32x10":
+        eng = cls.__new__(cls)
+        eng.key = state.key
+        eng.position = _position(state)
+        eng._ctr = (ctypes.c_uint32 * 4)()
+        return eng
+
+    @property
+    def state(self) -> PhiloxState:
+        return _state_at(self.key, self.position)
+
+    def skip_ahead(self, n: int) -> "Philox4x32x10":
+        if n < 0:
+            raise ValueError("skip count must be non-negative")
+        self.position = (self.position + n) % (1 << 130)
+        return self
+
+    def launch_args(self):
+        blk = self.position >> 2
+        c = self._ctr
+        c[0] = blk & MASK32
+        c[1] = (blk >> 32) & MASK32
+        c[2] = (blk >> 64) & MASK32
+        c[3] = (blk >> 96) & MASK32
+        return (self.key[0] & MASK32, self.key[1] & MASK32, c, self.position & 3)
+
+
+class Mrg32k3a:
+    """oneMKL-style stateful MRG32k3a engine (`oneapi::mkl::rng::mrg32k3a`)."""
+
+    kind = EngineKind.MRG32K3A
+
+    def __init__(self, seed: int = 0, offset: int = 0):
+        st = seed_engine(EngineKind.MRG32K3A, seed)
+        self._set(st.s1, st.s2)
+        if offset:
+            self.skip_ahead(offset)
+
+    def _set(self, s1, s2):
+        self._s1 = _lib.u32_array(s1)
+        self._s2 = _lib.u32_array(s2)
+
+    @classmethod
+    def from_state(cls, state: Mrg32k3aState) -> "Mrg32k3a":
+        eng = cls.__new__(cls)
+        eng._set(state.s1, state.s2)
+        return eng
+
+    @property
+    def state(self) -> Mrg32k3aState:
+        return Mrg32k3aState(tuple(self._s1), tuple(self._s2))
+
+    def skip_ahead(self, n: int) -> "Mrg32k3a":
+        if n < 0:
+            raise ValueError("skip count must be non-negative")
+        if n:
+            _lib.check(_lib.lib.prng_mrg32k3a_skip_ahead(self._s1, self._s2, n & MASK64, (n >> 64) & MASK64,
+                                                         self._s1, self._s2))
+        return self
+
+    def launch_args(self):
+        return (self._s1, self._s2)
+
+
+Engine = Union[Philox4x32x10, Mrg32k3a]

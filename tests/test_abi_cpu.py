@@ -147,3 +147,19 @@ def test_segment_table_chains_positions():
     assert pos == [(1 << 96) + 5, (1 << 96) + 200005, (1 << 96) + 200008]
     assert tab["out_offset"].tolist() == [0, 200000, 200003]
     assert calosim.allocation(4000) == 200000 and calosim.allocation(70000) == 210000
+
+
+def test_onemkl_style_engines_track_reference_positions():
+    eng = P.Philox4x32x10(777, offset=5)
+    assert eng.state == P.skip_ahead(P.seed_engine(P.EngineKind.PHILOX4X32X10, 777), 5)
+    eng.skip_ahead(1 << 100)
+    assert P.stream_position(eng.state) == 5 + (1 << 100)
+    back = P.Philox4x32x10.from_state(eng.state)
+    assert back.position == eng.position and back.key == eng.key
+    k0, k1, ctr, lane = eng.launch_args()
+    blk = eng.position >> 2
+    assert list(ctr) == [(blk >> (32 * i)) & 0xFFFFFFFF for i in range(4)] and lane == eng.position & 3
+    m = P.Mrg32k3a(4242, offset=1000)
+    assert m.state == P.skip_ahead(P.seed_engine(P.EngineKind.MRG32K3A, 4242), 1000)
+    with pytest.raises(ValueError):
+        m.skip_ahead(-1)

@@ -451,3 +451,15 @@ def test_bad_output_buffers_are_rejected():
     rc = _lib.lib.prng_philox4x32x10_bits(k0, k1, ctr, lane, 16, pageable.ctypes.data, None)
     assert rc in (_lib.PRNG_ERR_INVALID_PARAMETER, _lib.PRNG_ERR_CUDA)
     assert _lib.lib.prng_last_error()
+
+
+def test_onemkl_engine_objects_stream_like_states():
+    """generate(distr, engine, n, out) on stateful engines == chained
+    immutable-state requests (oneMKL semantics: the engine advances)."""
+    for eng, st in ((P.Philox4x32x10(99), P.seed_engine(PHILOX, 99)), (P.Mrg32k3a(99), P.seed_engine(MRG, 99))):
+        for spec, n in ((P.Uniform(-1.0, 1.0), 1001), (P.Gaussian(0.0, 1.0), 777), (P.UniformBits(), 5)):
+            ret, a = P.generate(spec, eng, n)
+            assert ret is eng
+            st, b = P.generate(spec, st, n)
+            assert torch.equal(a, b)
+            assert eng.state == st
