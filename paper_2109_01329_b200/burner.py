@@ -1,0 +1,181 @@
+"""RNG burner on the GPU: timed generate ->
+transform -> copy-back cycles with the reference's result format.
+
+Mirrors pkg/src/portarng/rngburn.py: `burn_once` is one time-to-solution
+cycle as the paper defines it (construction, allocation,
+generation, range transform, synchronisation, device-to-host copy), the API
+modes keep the reference's names, and results are written in its exact CSV
+schema (rngburn.py:34, 183-192) so `portarng.rngburn.compare` can compute
+slowdowns and P between a GPU file and a CPU file.
+
+API modes on CUDA:
+* ``"buffer"``  -- two kernels (generate unit values, then the range
+  transform) ordered implicitly by one stream: the accessor-inferred RAW edge
+  of the reference's buffer mode (execution.py:222-272, rngburn.py:142-144);
+* ``"usm"``     -- the same two kernels on two streams with an explicit CUDA
+  event dependency: the reference's event-list USM mode (execution.py:274-302,
+  rngburn.py:145-147);
+* ``"hostdirect"`` -- the fused single-kernel library call (the native-baseline
+  role, rngburn.py:127-133).
+All three produce bit-identical output (tests/test_burner.py).
+"""
+
+from __future__ import annotations
+
+import csv
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+from . import _lib
+from .distributions import Gaussian, Uniform, generate
+from .engine import EngineKind, _stream_handle, _torch, seed_engine
+from .errors import Error, InvalidParameter
+
+CSV_HEADER = ["platform", "api", "backend", "engine", "dist", "batch", "iter", "tts_ns"]  # rngburn.py:34
+API_MODES = ("buffer", "usm", "hostdirect")
+
+
+class ConfigError(Error):
+    """Malformed benchmark configuration (portarng.errors.ConfigError)."""
+
+
+class SchemaMismatch(Error):
+    """CSV file does not carry the expected header (portarng.errors.SchemaMismatch)."""
+
+
+def dist_label(spec) -> str:
+    """distributions.py:156-160."""
+    if isinstance(spec, Uniform):
+        return f"uniform:{spec.lo:g}:{spec.hi:g}"
+    return f"gaussian:{spec.mean:g}:{spec.stddev:g}"
+
+
+@dataclass
+class RunRecord:
+    """metrics.py:23-39 (same fields)."""
+
+    platform: str
+    api_mode: str
+    backend: str
+    engine: str
+    dist: str
+    batch: int
+    samples: List[int] = field(default_factory=list)
+
+
+@dataclass
+class BurnConfig:
+    """rngburn.py:41-59 with the CPU backend replaced by a CUDA device."""
+
+    engine: EngineKind
+    dist: object
+    api_mode: str
+    batches: List[int]
+    iterations: int = 100
+    seed: int = 0
+    out_path: Optional[str] = None
+    platform: str = "b200"
+    device: str = "cuda:0"
+
+    def __post_init__(self):
+        if self.api_mode not in API_MODES:
+            raise ConfigError(f"api mode must be one of {API_MODES}, got {self.api_mode!r}")
+        if not self.batches or any(b < 1 for b in self.batches):
+            raise ConfigError(f"batch sizes must be >= 1, got {self.batches}")
+        if self.iterations < 1:
+            raise ConfigError(f"iterations must be >= 1, got {self.iterations}")
+
+
+def _transform_range(spec) -> Tuple[float, float]:
+    # rngburn.py:103-108: gaussian batches keep an identity transform
+    return (spec.lo, spec.hi) if isinstance(spec, Uniform) else (0.0, 1.0)
+
+
+def _range_fn(precision):
+    return _lib.lib.prng_range_transform_f32 if precision == "fp32" else _lib.lib.prng_range_transform_f64
+
+
+def burn_once(engine: EngineKind, spec, api_mode: str, batch: int, seed: int, device: str = "cuda:0",
+              _streams=None) -> Tuple[int, object]:
+    """One timed full cycle on the GPU; returns (tts_ns, host numpy array).  rngburn.py:111-151."""
+    torch = _torch()
+    if api_mode not in API_MODES:
+        raise ConfigError(f"api mode must be one of {API_MODES}, got {api_mode!r}")
+    if not isinstance(spec, (Uniform, Gaussian)):
+        raise InvalidParameter("the burner runs uniform or gaussian requests")
+    lo, hi = _transform_range(spec)
+    dev = torch.device(device)
+    s0 = torch.cuda.current_stream(dev)
+    t0 = time.perf_counter_ns()
+    state = seed_engine(engine, seed)
+    buf = torch.empty(batch, dtype=torch.float32 if spec.precision == "fp32" else torch.float64, device=dev)
+    if api_mode == "hostdirect":
+        generate(spec, state, batch, out=buf, stream=s0)
+        if isinstance(spec, Gaussian):  # identity transform, as the reference applies it
+            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(s0)))
+    else:
+        unit = Uniform(0.0, 1.0, spec.precision) if isinstance(spec, Uniform) else spec
+        if api_mode == "buffer":
+            generate(unit, state, batch, out=buf, stream=s0)
+            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(s0)))
+        else:  # usm: producer / consumer streams joined by an explicit event
+            sa, sb = _streams if _streams is not None else (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+            sa.wait_stream(s0)
+            generate(unit, state, batch, out=buf, stream=sa)
+            ev = torch.cuda.Event()
+            ev.record(sa)
+            sb.wait_event(ev)
+            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(sb)))
+            s0.wait_stream(sb)
+            buf.record_stream(sa)
+            buf.record_stream(sb)
+    host = buf.cpu().numpy()  # D2H on s0 (synchronous)
+    tts = time.perf_counter_ns() - t0
+    return tts, host
+
+
+def run_burner(config: BurnConfig) -> List[RunRecord]:
+    """rngburn.py:154-177: every batch size, `iterations` cycles each."""
+    torch = _torch()
+    dev = torch.device(config.device)
+    streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    backend = f"cuda:{torch.cuda.get_device_properties(dev).multi_processor_count}sm"
+    records = []
+    for batch in config.batches:
+        samples = []
+        for _ in range(config.iterations):
+            tts, _ = burn_once(config.engine, config.dist, config.api_mode, batch, config.seed, config.device,
+                               streams)
+            samples.append(tts)
+        records.append(RunRecord(config.platform, config.api_mode, backend, config.engine.value,
+                                 dist_label(config.dist), batch, samples))
+    if config.out_path:
+        write_records_csv(records, config.out_path)
+    return records
+
+
+def write_records_csv(records: Sequence[RunRecord], path: str) -> None:
+    """Byte-compatible with rngburn.write_records_csv (rngburn.py:183-192)."""
+    with open(path, "w", newline="") as f:
+        writer = csv.writer(f, lineterminator="\n")
+        writer.writerow(CSV_HEADER)
+        for rec in records:
+            for it, tts in enumerate(rec.samples):
+                writer.writerow([rec.platform, rec.api_mode, rec.backend, rec.engine, rec.dist, rec.batch, it, tts])
+
+
+def read_rows_csv(path: str) -> List[dict]:
+    """rngburn.read_rows_csv (rngburn.py:195-217): exact header enforced."""
+    with open(path, newline="") as f:
+        reader = csv.reader(f)
+        header = next(reader, None)
+        if header != CSV_HEADER:
+            raise SchemaMismatch(f"{path}: expected header {CSV_HEADER}, got {header}")
+        rows = []
+        for row in reader:
+            if len(row) != len(CSV_HEADER):
+                raise SchemaMismatch(f"{path}: malformed row {row!r}")
+            rows.append({"platform": row[0], "api": row[1], "backend": row[2], "engine": row[3], "dist": row[4],
+                         "batch": int(row[5]), "iter": int(row[6]), "tts_ns": int(row[7])})
+    return rows

@@ -206,6 +206,18 @@ def main():
                        "final_position": int(__import__("portarng").engine.stream_position(st))}
     g["calosim"] = calo
 
+    # Burner result file format (rngburn.write_records_csv, rngburn.py:183-192).
+    import tempfile
+
+    from portarng.metrics import RunRecord as RefRecord
+    from portarng.rngburn import write_records_csv
+
+    recs = [RefRecord("b200", "buffer", "cuda:148sm", "philox", "uniform:-1:1", 1000, [1500, 1400, 1450]),
+            RefRecord("b200", "usm", "cuda:148sm", "mrg32k3a", "gaussian:2:0.5", 7, [99])]
+    with tempfile.NamedTemporaryFile("r", suffix=".csv") as tmp:
+        write_records_csv(recs, tmp.name)
+        g["burner_csv"] = open(tmp.name).read()
+
     for case in CASES:
         arrays[f"case__{case[0]}"] = run_case(case)
     g["cases"] = [list(c) for c in CASES]
