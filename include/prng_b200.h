@@ -126,6 +126,38 @@ typedef struct prng_segment {
 int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng_segment_t *segs, uint32_t nseg,
                                             uint64_t max_count, double a, double b, float *out, void *stream);
 
+/* ---- FastCaloSim-style deposition consumer (calosim.simulate_event,
+ *      calosim.py:313-347), bit-identical to the reference's numpy
+ *      arithmetic.  All arrays are device memory. ---- */
+#define PRNG_CALO_MAX_BINS 16
+typedef struct prng_calo_particle {
+    uint64_t batch_offset; /* first of its 3*hits uniforms in the packed batch buffer */
+    uint64_t hit_offset;   /* first of its hits in the per-hit arrays              */
+    uint32_t hits;         /* m (calosim.py:296-300)                                */
+    uint32_t region;       /* _particle_region (calosim.py:259-262)                 */
+    uint32_t param;        /* index into the parameterization table                 */
+    uint32_t pad;
+    double target;         /* energy * sampling_fraction                            */
+} prng_calo_particle_t;
+typedef struct prng_calo_param {
+    double bin_edges[PRNG_CALO_MAX_BINS + 1];
+    double cumw[PRNG_CALO_MAX_BINS]; /* np.cumsum(weights) */
+    uint32_t nbins;
+    uint32_t pad;
+} prng_calo_param_t;
+/* Per hit: cell id and raw energy, then per particle the pairwise-summed
+ * normalisation to amounts (in place) and the particle sums. */
+int prng_calo_hits(const float *batch, const prng_calo_particle_t *particles, uint32_t nparticles,
+                   const uint32_t *region_offsets, const uint32_t *region_cells, const prng_calo_param_t *params,
+                   uint32_t *hit_cell, double *hit_amount, double *particle_sums, void *stream);
+/* Per event (hits [event_hit_offsets[e], event_hit_offsets[e+1])): unique
+ * cells ascending with their sequentially summed amounts, written at the
+ * event's hit offset; dep_count[e] = number of unique cells. */
+size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents);
+int prng_calo_deposit(const uint32_t *hit_cell, const double *hit_amount, uint64_t total_hits,
+                      const uint64_t *event_hit_offsets, uint32_t nevents, void *scratch, size_t scratch_bytes,
+                      uint32_t *dep_cell, double *dep_energy, uint32_t *dep_count, void *stream);
+
 /* ---- Host-buffer drop-ins for the reference kernel plugin
  *      (portarng._kernels: philox_fill / mrg_fill / box_muller,
  *      _kernels/__init__.py:24-27).  Synchronous; generate on the current

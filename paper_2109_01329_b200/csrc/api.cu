@@ -37,6 +37,13 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
+}  // namespace
+
+// Shared with the other translation units (calo.cu): one error slot per thread.
+int prng_detail_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+
+namespace {
+
 int cuda_fail(cudaError_t e, const char* what) {
     return fail(PRNG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }

@@ -186,24 +186,33 @@ def main():
     # per-event hits, allocations and the first uniforms of each device batch.
     from portarng import calosim as C
 
-    geo = C.synth_geometry(2000, C.DEFAULT_REGIONS)
+    geo = C.synth_geometry(20000, C.DEFAULT_REGIONS)
+    for r, ids in enumerate(geo.region_cell_ids):
+        arrays[f"calo_geom__{r:02d}"] = np.asarray(ids, dtype=np.int64)
     calo = {}
-    for label, scen, nev, min_batch in (("electron", C.ScenarioKind.SINGLE_ELECTRON, 40, C.DEFAULT_MIN_BATCH),
-                                        ("ttbar_small_batch", C.ScenarioKind.TTBAR, 3, 1000)):
+    for label, scen, nev, min_batch, sf in (
+            ("electron", C.ScenarioKind.SINGLE_ELECTRON, 40, C.DEFAULT_MIN_BATCH, 1.0),
+            ("ttbar_small_batch", C.ScenarioKind.TTBAR, 3, 1000, 0.25)):
         params = C.synth_params(scen)
         evs = C._synth_events(scen, nev, 777, params)
         st = seed_engine(P, 777)
         rows = []
-        for ev in evs:
-            pos = st.counter, st.lane_index
-            st2, res = C.simulate_event(ev, geo, params, st, min_batch=min_batch)
+        for e, ev in enumerate(evs):
+            st2, res = C.simulate_event(ev, geo, params, st, min_batch=min_batch, sampling_fraction=sf)
             first = D.fill_uniform_unit(st, 4, "fp32")[1].values
             rows.append({"hit_ranges": [[params[p.kind].hit_lo, params[p.kind].hit_hi] for p in ev.particles],
+                         "particles": [[p.kind, p.energy, list(p.direction)] for p in ev.particles],
                          "hits": res.hits, "allocated": res.randoms_allocated,
+                         "particle_sums": [float(x) for x in res.particle_sums],
                          "first4": [float(x) for x in first]})
+            cells = np.asarray(sorted(res.deposits), dtype=np.int64)
+            arrays[f"calo__{label}__{e:03d}__cells"] = cells
+            arrays[f"calo__{label}__{e:03d}__sums"] = np.asarray([res.deposits[c] for c in cells.tolist()])
             st = st2
-        calo[label] = {"min_batch": min_batch, "events": rows,
-                       "final_position": int(__import__("portarng").engine.stream_position(st))}
+        calo[label] = {"min_batch": min_batch, "sampling_fraction": sf, "events": rows,
+                       "final_position": int(__import__("portarng").engine.stream_position(st)),
+                       "params": {k: {"hit_lo": p.hit_lo, "hit_hi": p.hit_hi, "bin_edges": p.bin_edges.tolist(),
+                                      "weights": p.weights.tolist()} for k, p in params.items()}}
     g["calosim"] = calo
 
     # Burner result file format (rngburn.write_records_csv, rngburn.py:183-192).

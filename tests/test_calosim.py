@@ -46,6 +46,36 @@ def test_batches_start_where_reference_batches_start(golden):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("label", ["electron", "ttbar_small_batch"])
+def test_gpu_deposition_bit_identical_to_reference(golden, golden_arrays, label):
+    """simulate_events (control draws, one segment launch, hit kernel,
+    pairwise normalisation, segmented sort + run sums) == the reference's
+    simulate_event deposits, particle sums and accounting, exactly."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_01329_b200 as P
+
+    ref = golden["calosim"][label]
+    nreg = len([k for k in golden_arrays if k.startswith("calo_geom__")])
+    geom = [golden_arrays[f"calo_geom__{r:02d}"] for r in range(nreg)]
+    params = {k: C.Parameterization(k, v["hit_lo"], v["hit_hi"], v["bin_edges"], v["weights"])
+              for k, v in ref["params"].items()}
+    det = C.Detector(geom, params)
+    events = [[C.Particle(k, e, tuple(d)) for k, e, d in ev["particles"]] for ev in ref["events"]]
+    st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+    final, results = C.simulate_events(events, det, st, ref["min_batch"], ref["sampling_fraction"])
+    assert P.stream_position(final) == ref["final_position"]
+    for e, (res, want) in enumerate(zip(results, ref["events"])):
+        assert res.hits == want["hits"] and res.randoms_allocated == want["allocated"]
+        assert res.particle_sums == want["particle_sums"], e
+        cells = golden_arrays[f"calo__{label}__{e:03d}__cells"]
+        sums = golden_arrays[f"calo__{label}__{e:03d}__sums"]
+        assert sorted(res.deposits) == cells.tolist(), e
+        assert [res.deposits[c] for c in cells.tolist()] == sums.tolist(), e
+
+
+@pytest.mark.gpu
 def test_gpu_plan_segments_and_graph(golden):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
