@@ -44,6 +44,7 @@ WORKLOADS = {
     "c3_gauss": ("philox", "gaussian", "fp32", 1 << 30, "philox4x32x10 seed=777 gaussian fp32 (0,1) (C3)"),
     "c3_logn": ("philox", "lognormal", "fp32", 1 << 30, "philox4x32x10 seed=777 lognormal fp32 (0,1) (C3)"),
     "c5": ("philox", "uniform", "fp32", 0, "FastCaloSim-style ~10^4 x 200k fp32 batches (C5)"),
+    "c5_full": ("philox", "uniform", "fp32", 0, "FastCaloSim single-electron run incl. deposition (C5)"),
 }
 METRIC = "Gsamples/s (and % HBM-write roofline) for Philox uniform fp32 at 1/2/4/8 B200"
 KERNEL_NAMES = {
@@ -242,6 +243,93 @@ def run_sweep(P, torch, st, dev, world, tdist, max_log2):
         del out
         torch.cuda.empty_cache()
     return rows
+
+
+def run_c5_full(args):
+    """C5 end to end: FastCaloSim single-electron run (control draws, per-event
+    200k-uniform batches, hit deposition) on the GPU vs the reference's
+    per-event CPU path (oracle restatement, 1 thread like its Serial backend)."""
+    import numpy as np
+    import torch
+
+    import paper_2109_01329_b200 as P
+    from paper_2109_01329_b200 import calosim as C
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    nev, regions, ncells = args.events, 24, 190_000  # calosim.py:48-50 defaults
+    geom = [np.arange(r, ncells, regions, dtype=np.int64) for r in range(regions)]  # synth_geometry round-robin
+    edges = np.linspace(0.001, 0.101, 9)
+    weights = np.asarray([0.05, 0.10, 0.20, 0.25, 0.20, 0.10, 0.07, 0.03])  # synth_params (calosim.py:156-164)
+    det = C.Detector(geom, {"electron": C.Parameterization("electron", 4000, 6500, edges, weights)})
+    events = C.synth_single_electron_events(nev, 777)
+    st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+    C.simulate_events(events[:50], det, st, dicts=False)  # warm-up
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        final, res = C.simulate_events(events, det, st, dicts=False)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    sec = statistics.median(ts)
+    total_hits = int(sum(res["hits"]))
+    cpu = None
+    if not args.no_cpu:
+        from oracle import calo_cpu
+        from oracle.cpu_baseline import CpuPath
+
+        c = CpuPath(workers=1)
+        sample = min(nev, 100)
+        params = {"electron": (edges, weights)}
+        per_particle = []
+        hits, allocs = C.plan_from_controls(0, [[(4000, 6500)]] * sample, C.DEFAULT_MIN_BATCH,
+                                            *_cpu_control_draws(c), per_particle=per_particle)
+        buf = np.empty(C.DEFAULT_MIN_BATCH, dtype=np.float32)
+        t0 = time.perf_counter()
+        pos = 0
+        for e in range(sample):
+            c.burn_philox_uniform((777, 0), pos, allocs[e], out=buf)
+            parts = [(p.kind, p.energy, p.direction) for p in events[e]]
+            calo_cpu.deposit_event(buf, parts, per_particle[e], geom, params, regions)
+            pos += allocs[e]
+        cpu_sec = (time.perf_counter() - t0) / sample
+        c.close()
+        cpu = {"value": 1.0 / cpu_sec, "unit": "events/s", "cores": 1, "kind": c.kind,
+               "sample": f"{sample} single-electron events: 200k-uniform batch (reference core) + numpy deposition "
+                         f"restated from calosim.py:313-347, Serial"}
+    line = {
+        "metric": "FastCaloSim single-electron events/s (control draws + batch generation + deposition)",
+        "value": nev / sec, "unit": "events/s", "n_gpus": 1, "steps": len(ts), "warmup": 1,
+        "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32->fp32 (fp64 deposition)", "data": "synthetic single-electron events (seed 777)",
+        "config": {"workload": f"{nev} events, 190000 cells / 24 regions, min_batch 200000",
+                   "total_hits": total_hits, "timing": "wall clock of simulate_events incl. planning, "
+                                                       "segment launch, deposition kernels and D2H of results"},
+        "e2e": {"value": nev / sec, "unit": "events/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(res["cells"].nbytes + res["energy"].nbytes)},
+        "cpu_baseline": cpu, "gpu_launches": 5,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _cpu_control_draws(c):
+    """Control-word draws for the CPU path (reference core words -> unit floats)."""
+    import numpy as np
+
+    from oracle import oracle as O
+
+    def batched(positions, counts):
+        return np.concatenate([O.words_to_unit(c._philox_fill((777, 0), p, n), "fp32").astype(np.float64)
+                               for p, n in zip(positions, counts)])
+
+    def one(position, count):
+        return O.words_to_unit(c._philox_fill((777, 0), position, count), "fp32").astype(np.float64)
+
+    return batched, one
 
 
 def run_c5(args):
@@ -505,6 +593,8 @@ def main():
         return run_reference(args)
     if args.workload == "c5":
         return run_c5(args)
+    if args.workload == "c5_full":
+        return run_c5_full(args)
     return run_ours(args)
 
 

@@ -45,6 +45,32 @@ def test_batches_start_where_reference_batches_start(golden):
         pos += e["allocated"]
 
 
+@pytest.mark.parametrize("label", ["electron", "ttbar_small_batch"])
+def test_cpu_deposition_oracle_matches_reference(golden, golden_arrays, label):
+    """oracle/calo_cpu.py (the C5 CPU baseline) reproduces the reference's
+    simulate_event deposits from oracle-generated batches."""
+    from oracle import calo_cpu
+
+    ref = golden["calosim"][label]
+    nreg = len([k for k in golden_arrays if k.startswith("calo_geom__")])
+    geom = [golden_arrays[f"calo_geom__{r:02d}"] for r in range(nreg)]
+    params = {k: (np.asarray(v["bin_edges"]), np.asarray(v["weights"])) for k, v in ref["params"].items()}
+    key = O.seed_philox(777)
+    ranges = [[tuple(r) for r in e["hit_ranges"]] for e in ref["events"]]
+    pp = []
+    C.plan_from_controls(0, ranges, ref["min_batch"], *_oracle_draws(key), per_particle=pp)
+    pos = 0
+    for e, ev in enumerate(ref["events"][:6]):
+        batch = O.words_to_unit(O.philox_words(key, pos, ev["allocated"]), "fp32")
+        dep, psums = calo_cpu.deposit_event(batch, ev["particles"], pp[e], geom, params, nreg,
+                                            ref["sampling_fraction"])
+        assert psums == ev["particle_sums"]
+        cells = golden_arrays[f"calo__{label}__{e:03d}__cells"]
+        assert sorted(dep) == cells.tolist()
+        assert [dep[c] for c in cells.tolist()] == golden_arrays[f"calo__{label}__{e:03d}__sums"].tolist()
+        pos += ev["allocated"]
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("label", ["electron", "ttbar_small_batch"])
 def test_gpu_deposition_bit_identical_to_reference(golden, golden_arrays, label):
