@@ -167,6 +167,47 @@ __device__ __forceinline__ uint32_t mrg_step_mixed(MrgStateMixed& s) {
     return p1 >= p2 ? p1 - p2 : p1 - p2 + kMrgM1;
 }
 
+// All-fp64 formulation (L'Ecuyer's floating-point MRG32k3a with symmetric
+// residues).  Each component keeps its window as integers in [-m/2 - 1,
+// m/2 + 1] held in doubles, so a*x_i - b*x_j stays below 2^52.1 and is exact
+// (DMUL + DFMA); the reduction r = p - rint(p/m)*m (DFMA with the 1.5*2^52
+// rounding magic, DADD, DFMA) is exact and lands back in the symmetric range.
+// Both components run on the FP64 pipe with no compare/select in the
+// recurrence; only the output word is canonicalised, in 32-bit integers:
+// the magic-added double's low word is the residue's two's complement,
+// c = r < 0 ? r + m : r, z = (c1 - c2) mod m1 (_core.pyx:85-101).
+struct MrgStateF64 {
+    double x10, x11, x12, x20, x21, x22;
+};
+
+__host__ __device__ inline double mrg_sym(uint32_t x, uint32_t m) {
+    return x > m / 2 ? (double)x - (double)m : (double)x;
+}
+
+constexpr double kRintMagic = 6755399441055744.0;  // 1.5 * 2^52
+
+__device__ __forceinline__ double mrg_reduce(double p, double m, double inv_m) {
+    const double k = __dadd_rn(__fma_rn(p, inv_m, kRintMagic), -kRintMagic);
+    return __fma_rn(-k, m, p);
+}
+
+__device__ __forceinline__ uint32_t mrg_canon(double r, uint32_t m) {
+    const int32_t i = __double2loint(__dadd_rn(r, kRintMagic));
+    return (uint32_t)i + (i < 0 ? m : 0u);
+}
+
+__device__ __forceinline__ uint32_t mrg_step_f64(MrgStateF64& s) {
+    const double p1 = mrg_reduce(__fma_rn(-(double)kMrgA13N, s.x10, __dmul_rn((double)kMrgA12, s.x11)),
+                                 (double)kMrgM1, 1.0 / (double)kMrgM1);
+    const double p2 = mrg_reduce(__fma_rn(-(double)kMrgA23N, s.x20, __dmul_rn((double)kMrgA21, s.x22)),
+                                 (double)kMrgM2, 1.0 / (double)kMrgM2);
+    s.x10 = s.x11; s.x11 = s.x12; s.x12 = p1;
+    s.x20 = s.x21; s.x21 = s.x22; s.x22 = p2;
+    const uint32_t c1 = mrg_canon(p1, kMrgM1);
+    const uint32_t c2 = mrg_canon(p2, kMrgM2);
+    return c1 >= c2 ? c1 - c2 : c1 - c2 + kMrgM1;
+}
+
 // y = J x mod m (3x3), products folded before summation.
 template <uint32_t C>
 __device__ __forceinline__ void mat3_apply(const uint32_t* J, uint32_t& a, uint32_t& b, uint32_t& c) {
@@ -183,7 +224,22 @@ __device__ __forceinline__ void mat3_apply(const uint32_t* J, uint32_t& a, uint3
 
 // ---------------------------------------------------------- transforms
 // Word -> unit: (w >> 8) * 2^-24, exact in fp32 and fp64 (distributions.py:78-87).
+//
+// Without I2FP (which issues on the FMA-heavy pipe, already saturated by the
+// Philox IMAD.WIDEs): one funnel shift puts m = w >> 8 under the exponent
+// of 0.5, F = bits(0x3F000000 | m).  The top bit of m lands on the exponent's
+// LSB, so F = 0.5 + u when u < 0.5 and F = 2u when u >= 0.5 (u = m 2^-24),
+// and u = min(F - 0.5, F * 0.5): both candidates are exact and the smaller
+// is always the right one (exhaustively checked over all 2^24 m,
+// tools/check_unit_trick.c).
+#ifndef PRNG_UNIT_I2FP
+__device__ __forceinline__ float unit_f32(uint32_t w) {
+    const float f = __uint_as_float(__funnelshift_r(w, 0x3Fu, 8));
+    return fminf(__fadd_rn(f, -0.5f), __fmul_rn(f, 0.5f));
+}
+#else
 __device__ __forceinline__ float unit_f32(uint32_t w) { return __fmul_rn((float)(w >> 8), kUnitF); }
+#endif
 // 2^52 + (w >> 8) built from bits (no I2F.F64 on the XU pipe): the 24-bit
 // integer sits in the low mantissa bits of 2^52.
 __device__ __forceinline__ double u24_magic(uint32_t w) { return __hiloint2double(0x43300000, (int)(w >> 8)); }

@@ -20,6 +20,10 @@ namespace prng {
 
 constexpr int kMrgMaxBits = 32;
 constexpr int kMrgThreads = 128;
+#ifndef PRNG_MRG_MINB
+#define PRNG_MRG_MINB 6
+#endif
+constexpr int kMrgMinBlocks = PRNG_MRG_MINB;
 
 struct MrgLaunch {
     uint32_t s1[3], s2[3];
@@ -89,7 +93,7 @@ __device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ 
 }
 
 template <int X>
-__global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
+__global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const MrgLaunch a) {
     using T = typename XformTraits<X>::T;
     constexpr int TW = MrgTile<T>::kWords;
     constexpr int WARPS = kMrgThreads / 32;
@@ -115,10 +119,12 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
             mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
         }
     }
-    MrgStateMixed sa{x10, x11, x12, (double)x20, (double)x21, (double)x22};
+    MrgStateF64 sa{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
+                   mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
     mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
     mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
-    MrgStateMixed sb{x10, x11, x12, (double)x20, (double)x21, (double)x22};
+    MrgStateF64 sb{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
+                   mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
 
     const uint64_t half = a.chunk >> 1;
     T* __restrict__ out = static_cast<T*>(a.out);
@@ -135,18 +141,18 @@ __global__ void __launch_bounds__(kMrgThreads) mrg_kernel(const MrgLaunch a) {
             if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
                 for (int k = 0; k < CE; k += 2) {
-                    const uint32_t a0 = mrg_step_mixed(sa);
-                    const uint32_t b0 = mrg_step_mixed(sb);
-                    const uint32_t a1 = mrg_step_mixed(sa);
-                    const uint32_t b1 = mrg_step_mixed(sb);
+                    const uint32_t a0 = mrg_step_f64(sa);
+                    const uint32_t b0 = mrg_step_f64(sb);
+                    const uint32_t a1 = mrg_step_f64(sa);
+                    const uint32_t b1 = mrg_step_f64(sb);
                     xform2<X>(a0, a1, a.p, oa[k], oa[k + 1]);
                     xform2<X>(b0, b1, a.p, ob[k], ob[k + 1]);
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < CE; ++k) {
-                    const uint32_t wa = mrg_step_mixed(sa);
-                    const uint32_t wb = mrg_step_mixed(sb);
+                    const uint32_t wa = mrg_step_f64(sa);
+                    const uint32_t wb = mrg_step_f64(sb);
                     oa[k] = xform1<X>(wa, a.p);
                     ob[k] = xform1<X>(wb, a.p);
                 }
