@@ -151,12 +151,17 @@ int prng_calo_hits(const float *batch, const prng_calo_particle_t *particles, ui
                    const uint32_t *region_offsets, const uint32_t *region_cells, const prng_calo_param_t *params,
                    uint32_t *hit_cell, double *hit_amount, double *particle_sums, void *stream);
 /* Per event (hits [event_hit_offsets[e], event_hit_offsets[e+1])): unique
- * cells ascending with their sequentially summed amounts, written at the
- * event's hit offset; dep_count[e] = number of unique cells. */
+ * cells ascending with their sequentially summed amounts (np.unique +
+ * np.bincount), packed over all events: event e's deposits are
+ * dep_cell/dep_energy[dep_offsets[e] .. dep_offsets[e+1]) (dep_offsets has
+ * nevents + 1 entries; dep_offsets[nevents] = total deposits <= total_hits).
+ * cell_bits: every cell id is < 2^cell_bits (0 = 32); it bounds the radix
+ * passes of the per-event sort. */
 size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents);
 int prng_calo_deposit(const uint32_t *hit_cell, const double *hit_amount, uint64_t total_hits,
-                      const uint64_t *event_hit_offsets, uint32_t nevents, void *scratch, size_t scratch_bytes,
-                      uint32_t *dep_cell, double *dep_energy, uint32_t *dep_count, void *stream);
+                      const uint64_t *event_hit_offsets, uint32_t nevents, uint32_t cell_bits, void *scratch,
+                      size_t scratch_bytes, uint32_t *dep_cell, double *dep_energy, uint64_t *dep_offsets,
+                      void *stream);
 
 /* ---- Host-buffer drop-ins for the reference kernel plugin
  *      (portarng._kernels: philox_fill / mrg_fill / box_muller,

@@ -65,7 +65,7 @@ SIGNATURES = {
     "prng_philox4x32x10_uniform_f32_segments": ([_u32, _u32, _vp, _u32, _u64, _dbl, _dbl, _vp, _vp], _int),
     "prng_calo_hits": ([_vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "prng_calo_deposit_scratch_bytes": ([_u64, _u32], ctypes.c_size_t),
-    "prng_calo_deposit": ([_vp, _vp, _u64, _vp, _u32, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp], _int),
+    "prng_calo_deposit": ([_vp, _vp, _u64, _vp, _u32, _u32, _vp, ctypes.c_size_t, _vp, _vp, _vp, _vp], _int),
     "prng_kernels_philox_fill": ([_u32] * 7 + [_u64, _vp], _int),
     "prng_kernels_mrg_fill": ([_u32] * 6 + [_u64, _vp, _u32p, _u32p], _int),
     "prng_kernels_box_muller": ([_vp, _vp, _u64, _vp, _vp], _int),

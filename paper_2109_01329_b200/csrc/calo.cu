@@ -12,8 +12,10 @@
 //   * per event: deposits = np.unique + np.bincount over the particles' hits
 //     in order, i.e. cells sorted ascending and each cell's amounts summed
 //     sequentially in hit order: a stable segmented radix sort (CUB) by cell
-//     followed by one sequential run-sum per unique cell, compacted with a
-//     block scan.
+//     over the cell-id bits only, then one sequential run-sum per unique
+//     cell, compacted with a block scan into one packed array (a count pass,
+//     a device scan of the counts, a write pass) so the host copies back
+//     exactly the deposits.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -26,29 +28,28 @@ namespace {
 
 constexpr int kCaloThreads = 256;
 
-// numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src), float64.
-__device__ double np_pairwise_sum(const double* a, uint64_t n) {
+// numpy pairwise_sum (numpy/_core/src/umath/loops_utils.h.src), float64,
+// leaf branch (n <= PW_BLOCKSIZE = 128): n < 8 sequential; else eight
+// strided accumulators, combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
+// the remainder sequentially.  Larger n recurse on (n2, n - n2) with
+// n2 = n/2 rounded down to a multiple of 8 (combine_leaves below).
+__device__ double np_leaf_sum(const double* a, uint64_t n) {
     if (n < 8) {
         double res = 0.0;
         for (uint64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
         return res;
     }
-    if (n <= 128) {
-        double r[8];
+    double r[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) r[k] = a[k];
-        uint64_t i = 8;
-        for (; i < n - (n % 8); i += 8)
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    uint64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
 #pragma unroll
-            for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
-        double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-        return res;
-    }
-    uint64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    return __dadd_rn(np_pairwise_sum(a, n2), np_pairwise_sum(a + n2, n - n2));
+        for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
 }
 
 __global__ void __launch_bounds__(kCaloThreads)
@@ -76,38 +77,157 @@ __global__ void __launch_bounds__(kCaloThreads)
     }
 }
 
-// One thread per particle: raw_sum, in-place scaling to amounts, particle sum.
-__global__ void calo_normalize_kernel(const prng_calo_particle_t* __restrict__ parts, uint32_t nparts,
-                                      double* __restrict__ hit_amount, double* __restrict__ particle_sums) {
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= nparts) return;
+// numpy's pairwise sum evaluated by a warp: the recursion's leaves (runs of
+// <= 128 elements, each summed exactly as np_pairwise_sum's leaf branch) are
+// independent, so lane l sums leaves l, l + 32, ...; lane 0 then adds the leaf
+// sums back up the same binary tree.  Bit-identical to np_pairwise_sum.
+constexpr int kNormWarps = 4;
+constexpr int kNormMaxLeaves = 512;  // n <= ~28k per particle; larger: serial
+
+struct LeafRange {
+    uint64_t off, n;
+};
+
+__device__ __forceinline__ uint64_t pw_split(uint64_t n) {  // numpy: n2 = n / 2; n2 -= n2 % 8
+    const uint64_t n2 = n / 2;
+    return n2 - n2 % 8;
+}
+
+// Visit the leaves of np_pairwise_sum(a, n) in order: f(k, off, len); returns
+// the leaf count.  Iterative (explicit stack, depth <= log2(n / 64) + 1).
+template <typename F>
+__device__ __forceinline__ uint32_t for_each_leaf(uint64_t n, F f) {
+    LeafRange st[40];
+    int sp = 0;
+    uint32_t k = 0;
+    st[sp++] = LeafRange{0, n};
+    while (sp) {
+        const LeafRange r = st[--sp];
+        if (r.n <= 128) {
+            f(k++, r.off, r.n);
+            continue;
+        }
+        const uint64_t n2 = pw_split(r.n);
+        st[sp++] = LeafRange{r.off + n2, r.n - n2};
+        st[sp++] = LeafRange{r.off, n2};
+    }
+    return k;
+}
+
+// Sum the leaf values back up np_pairwise_sum's tree: res = left + right at
+// every internal node (iterative post-order walk); leaf(off, len) supplies
+// the value of each leaf, in order.
+template <typename L>
+__device__ double combine_leaves(uint64_t n, L leaf) {
+    struct Frame {
+        uint64_t off, n;
+        double left;
+        int stage;  // 0 = new, 1 = left child pending, 2 = right child pending
+    };
+    Frame st[40];
+    int sp = 0;
+    st[sp++] = Frame{0, n, 0.0, 0};
+    for (;;) {
+        Frame& t = st[sp - 1];
+        if (t.n > 128) {
+            t.stage = 1;
+            st[sp++] = Frame{t.off, pw_split(t.n), 0.0, 0};
+            continue;
+        }
+        double val = leaf(t.off, t.n);
+        --sp;
+        for (;;) {  // deliver val to the parents
+            if (sp == 0) return val;
+            Frame& p = st[sp - 1];
+            if (p.stage == 1) {
+                p.left = val;
+                p.stage = 2;
+                const uint64_t n2 = pw_split(p.n);
+                st[sp++] = Frame{p.off + n2, p.n - n2, 0.0, 0};
+                break;
+            }
+            val = __dadd_rn(p.left, val);
+            --sp;
+        }
+    }
+}
+
+// np_pairwise_sum(a, n) on one thread.
+__device__ double np_pairwise_sum(const double* a, uint64_t n) {
+    return combine_leaves(n, [&](uint64_t off, uint64_t len) { return np_leaf_sum(a + off, len); });
+}
+
+__device__ __forceinline__ uint32_t leaf_count(uint64_t n) {
+    return for_each_leaf(n, [](uint32_t, uint64_t, uint64_t) {});
+}
+
+__device__ double warp_pairwise_sum(const double* a, uint64_t n, double* leaf, uint32_t lane) {
+    for_each_leaf(n, [&](uint32_t k, uint64_t off, uint64_t len) {
+        if ((k & 31u) == lane) leaf[k] = np_leaf_sum(a + off, len);
+    });
+    __syncwarp();
+    double r = 0.0;
+    if (lane == 0) {
+        uint32_t k = 0;
+        r = combine_leaves(n, [&](uint64_t, uint64_t) { return leaf[k++]; });
+    }
+    __syncwarp();
+    return __shfl_sync(0xffffffffu, r, 0);
+}
+
+// One warp per particle: raw_sum, in-place scaling to amounts, particle sum.
+__global__ void __launch_bounds__(32 * kNormWarps)
+    calo_normalize_kernel(const prng_calo_particle_t* __restrict__ parts, uint32_t nparts,
+                          double* __restrict__ hit_amount, double* __restrict__ particle_sums) {
+    __shared__ double leaves[kNormWarps][kNormMaxLeaves];
+    const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const uint32_t p = blockIdx.x * kNormWarps + w;
+    if (p >= nparts) return;  // warp-uniform
     const prng_calo_particle_t pt = parts[p];
     if (pt.hits == 0) {
-        particle_sums[p] = 0.0;
+        if (lane == 0) particle_sums[p] = 0.0;
         return;
     }
     double* a = hit_amount + pt.hit_offset;
-    const double raw_sum = np_pairwise_sum(a, pt.hits);
+    const bool par = leaf_count(pt.hits) <= (uint32_t)kNormMaxLeaves;
+    double raw_sum;
+    if (par) {
+        raw_sum = warp_pairwise_sum(a, pt.hits, leaves[w], lane);
+    } else {
+        raw_sum = lane == 0 ? np_pairwise_sum(a, pt.hits) : 0.0;
+        raw_sum = __shfl_sync(0xffffffffu, raw_sum, 0);
+    }
     if (raw_sum > 0.0) {
         const double scale = pt.target / raw_sum;
-        for (uint32_t j = 0; j < pt.hits; ++j) a[j] = __dmul_rn(a[j], scale);
+        for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = __dmul_rn(a[j], scale);
     } else {
         const double each = pt.target / (double)pt.hits;  // np.full(m, target / m)
-        for (uint32_t j = 0; j < pt.hits; ++j) a[j] = each;
+        for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = each;
     }
-    particle_sums[p] = np_pairwise_sum(a, pt.hits);
+    __syncwarp();
+    double sum;
+    if (par) {
+        sum = warp_pairwise_sum(a, pt.hits, leaves[w], lane);
+    } else {
+        sum = lane == 0 ? np_pairwise_sum(a, pt.hits) : 0.0;
+    }
+    if (lane == 0) particle_sums[p] = sum;
 }
 
-// One CTA per event over its cell-sorted hits: run starts -> compacted
-// (cell, sequential run sum) at the event's offset.
+// One CTA per event over its cell-sorted hits.  COUNT pass: number of unique
+// cells per event.  WRITE pass: (cell, sequential run sum) compacted at the
+// event's packed offset dep_offsets[e] (exclusive scan of the counts).
+template <bool WRITE>
 __global__ void __launch_bounds__(kCaloThreads)
     calo_reduce_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ vals,
-                       const uint64_t* __restrict__ ev_off, uint32_t* __restrict__ dep_cell,
-                       double* __restrict__ dep_energy, uint32_t* __restrict__ dep_count) {
+                       const uint64_t* __restrict__ ev_off, uint64_t* __restrict__ counts,
+                       const uint64_t* __restrict__ dep_offsets, uint32_t* __restrict__ dep_cell,
+                       double* __restrict__ dep_energy) {
     using Scan = cub::BlockScan<uint32_t, kCaloThreads>;
     __shared__ typename Scan::TempStorage tmp;
     __shared__ uint32_t carry;
     const uint64_t beg = ev_off[blockIdx.x], end = ev_off[blockIdx.x + 1];
+    const uint64_t out0 = WRITE ? dep_offsets[blockIdx.x] : 0;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
     for (uint64_t base = beg; base < end; base += kCaloThreads) {
@@ -115,18 +235,18 @@ __global__ void __launch_bounds__(kCaloThreads)
         const uint32_t flag = (i < end && (i == beg || keys[i] != keys[i - 1])) ? 1u : 0u;
         uint32_t idx, total;
         Scan(tmp).ExclusiveSum(flag, idx, total);
-        if (flag) {
+        if (WRITE && flag) {
             const uint32_t key = keys[i];
             double s = 0.0;  // np.bincount: 0.0, then += weights in input order
             for (uint64_t k = i; k < end && keys[k] == key; ++k) s = __dadd_rn(s, vals[k]);
-            dep_cell[beg + carry + idx] = key;
-            dep_energy[beg + carry + idx] = s;
+            dep_cell[out0 + carry + idx] = key;
+            dep_energy[out0 + carry + idx] = s;
         }
         __syncthreads();
         if (threadIdx.x == 0) carry += total;
         __syncthreads();
     }
-    if (threadIdx.x == 0) dep_count[blockIdx.x] = carry;
+    if (!WRITE && threadIdx.x == 0) counts[blockIdx.x] = carry;
 }
 
 }  // namespace
@@ -156,49 +276,79 @@ int prng_calo_hits(const float* batch, const prng_calo_particle_t* particles, ui
     cudaStream_t s = (cudaStream_t)stream;
     calo_hits_kernel<<<nparticles, kCaloThreads, 0, s>>>(batch, particles, region_offsets, region_cells, params,
                                                          hit_cell, hit_amount);
-    calo_normalize_kernel<<<(nparticles + 127) / 128, 128, 0, s>>>(particles, nparticles, hit_amount,
-                                                                    particle_sums);
+    calo_normalize_kernel<<<(nparticles + kNormWarps - 1) / kNormWarps, 32 * kNormWarps, 0, s>>>(
+        particles, nparticles, hit_amount, particle_sums);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PRNG_OK : calo_fail(PRNG_ERR_CUDA, "calo hits: %s", cudaGetErrorString(e));
 }
 
-size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents) {
-    size_t temp = 0;
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+namespace {
+struct DepositScratch {
+    size_t keys, vals, counts, sort_temp, scan_temp, total;
+};
+
+DepositScratch deposit_layout(uint64_t total_hits, uint32_t nevents) {
+    size_t sort_temp = 0, scan_temp = 0;
+    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sort_temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                              (const double*)nullptr, (double*)nullptr, (int64_t)total_hits,
                                              (int64_t)nevents, (const uint64_t*)nullptr, (const uint64_t*)nullptr);
-    const size_t align = 256;
-    auto up = [&](size_t b) { return (b + align - 1) / align * align; };
-    return up(total_hits * sizeof(uint32_t)) + up(total_hits * sizeof(double)) + up(temp);
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (int64_t)nevents + 1);
+    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
+    DepositScratch d;
+    d.keys = up(total_hits * sizeof(uint32_t));
+    d.vals = up(total_hits * sizeof(double));
+    d.counts = up(((size_t)nevents + 1) * sizeof(uint64_t));
+    d.sort_temp = up(sort_temp);
+    d.scan_temp = up(scan_temp);
+    d.total = d.keys + d.vals + d.counts + d.sort_temp + d.scan_temp;
+    return d;
+}
+}  // namespace
+
+size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents) {
+    return deposit_layout(total_hits, nevents).total;
 }
 
 int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64_t total_hits,
-                      const uint64_t* event_hit_offsets, uint32_t nevents, void* scratch, size_t scratch_bytes,
-                      uint32_t* dep_cell, double* dep_energy, uint32_t* dep_count, void* stream) {
+                      const uint64_t* event_hit_offsets, uint32_t nevents, uint32_t cell_bits, void* scratch,
+                      size_t scratch_bytes, uint32_t* dep_cell, double* dep_energy, uint64_t* dep_offsets,
+                      void* stream) {
     if (nevents == 0) return PRNG_OK;
-    if (!hit_cell || !hit_amount || !event_hit_offsets || !dep_cell || !dep_energy || !dep_count)
+    if (!hit_cell || !hit_amount || !event_hit_offsets || !dep_cell || !dep_energy || !dep_offsets)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
-    const size_t need = prng_calo_deposit_scratch_bytes(total_hits, nevents);
-    if (!scratch || scratch_bytes < need)
-        return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", need);
+    if (cell_bits > 32) return calo_fail(PRNG_ERR_INVALID_PARAMETER, "cell_bits must be <= 32");
+    const DepositScratch L = deposit_layout(total_hits, nevents);
+    if (!scratch || scratch_bytes < L.total)
+        return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", L.total);
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t align = 256;
-    auto up = [&](size_t b) { return (b + align - 1) / align * align; };
     char* p = static_cast<char*>(scratch);
     uint32_t* keys_out = reinterpret_cast<uint32_t*>(p);
-    p += up(total_hits * sizeof(uint32_t));
+    p += L.keys;
     double* vals_out = reinterpret_cast<double*>(p);
-    p += up(total_hits * sizeof(double));
-    size_t temp = scratch_bytes - (size_t)(p - static_cast<char*>(scratch));
+    p += L.vals;
+    uint64_t* counts = reinterpret_cast<uint64_t*>(p);
+    p += L.counts;
+    void* sort_temp = p;
+    p += L.sort_temp;
+    void* scan_temp = p;
+    size_t sort_bytes = L.sort_temp, scan_bytes = L.scan_temp;
+    const int end_bit = cell_bits == 0 ? 32 : (int)cell_bits;  // keys < 2^cell_bits: fewer radix passes
     if (total_hits) {
-        cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(p, temp, hit_cell, keys_out, hit_amount, vals_out,
-                                                                 (int64_t)total_hits, (int64_t)nevents,
-                                                                 event_hit_offsets, event_hit_offsets + 1, 0, 32, s);
+        cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(sort_temp, sort_bytes, hit_cell, keys_out,
+                                                                 hit_amount, vals_out, (int64_t)total_hits,
+                                                                 (int64_t)nevents, event_hit_offsets,
+                                                                 event_hit_offsets + 1, 0, end_bit, s);
         if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "segmented sort: %s", cudaGetErrorString(e));
     }
-    calo_reduce_kernel<<<nevents, kCaloThreads, 0, s>>>(keys_out, vals_out, event_hit_offsets, dep_cell,
-                                                        dep_energy, dep_count);
-    cudaError_t e = cudaGetLastError();
+    cudaMemsetAsync(counts + nevents, 0, sizeof(uint64_t), s);
+    calo_reduce_kernel<false><<<nevents, kCaloThreads, 0, s>>>(keys_out, vals_out, event_hit_offsets, counts,
+                                                               nullptr, nullptr, nullptr);
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_temp, scan_bytes, counts, dep_offsets, (int64_t)nevents + 1, s);
+    if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "offset scan: %s", cudaGetErrorString(e));
+    calo_reduce_kernel<true><<<nevents, kCaloThreads, 0, s>>>(keys_out, vals_out, event_hit_offsets, nullptr,
+                                                              dep_offsets, dep_cell, dep_energy);
+    e = cudaGetLastError();
     return e == cudaSuccess ? PRNG_OK : calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(e));
 }
 
