@@ -8,16 +8,16 @@ modes keep the reference's names, and results are written in its exact CSV
 schema (rngburn.py:34, 183-192) so `portarng.rngburn.compare` can compute
 slowdowns and P between a GPU file and a CPU file.
 
-API modes on CUDA:
-* ``"buffer"``  -- two kernels (generate unit values, then the range
-  transform) ordered implicitly by one stream: the accessor-inferred RAW edge
-  of the reference's buffer mode (execution.py:222-272, rngburn.py:142-144);
-* ``"usm"``     -- the same two kernels on two streams with an explicit CUDA
-  event dependency: the reference's event-list USM mode (execution.py:274-302,
-  rngburn.py:145-147);
+API modes on CUDA (rngburn.py:127-149), through the CUDA task graph
+(execution.py in this package):
+* ``"buffer"``  -- generate and range-transform tasks submitted with
+  read_write accessors; the inferred RAW edge orders them;
+* ``"usm"``     -- the same two tasks with an explicit event dependency;
 * ``"hostdirect"`` -- the fused single-kernel library call (the native-baseline
-  role, rngburn.py:127-133).
-All three produce bit-identical output (tests/test_burner.py).
+  role), then the identity transform for gaussians as the reference applies it.
+The backend (Serial / Parallel(workers) / Graph(workers)) maps the graph onto
+one stream, a stream pool, or a replayed CUDA graph.  All combinations
+produce bit-identical output (tests/test_burner.py).
 """
 
 from __future__ import annotations
@@ -31,13 +31,11 @@ from . import _lib
 from .distributions import Gaussian, Uniform, generate
 from .engine import EngineKind, _stream_handle, _torch, seed_engine
 from .errors import Error, InvalidParameter
+from .execution import (AccessMode, Backend, ConfigError, Serial, TaskGraph, affine_kernel, backend_label,
+                        gaussian_generate_kernel, uniform_generate_kernel)
 
 CSV_HEADER = ["platform", "api", "backend", "engine", "dist", "batch", "iter", "tts_ns"]  # rngburn.py:34
 API_MODES = ("buffer", "usm", "hostdirect")
-
-
-class ConfigError(Error):
-    """Malformed benchmark configuration (portarng.errors.ConfigError)."""
 
 
 class SchemaMismatch(Error):
@@ -66,11 +64,12 @@ class RunRecord:
 
 @dataclass
 class BurnConfig:
-    """rngburn.py:41-59 with the CPU backend replaced by a CUDA device."""
+    """rngburn.py:41-59 (backend = a CUDA task-graph backend)."""
 
     engine: EngineKind
     dist: object
     api_mode: str
+    backend: Backend
     batches: List[int]
     iterations: int = 100
     seed: int = 0
@@ -92,12 +91,8 @@ def _transform_range(spec) -> Tuple[float, float]:
     return (spec.lo, spec.hi) if isinstance(spec, Uniform) else (0.0, 1.0)
 
 
-def _range_fn(precision):
-    return _lib.lib.prng_range_transform_f32 if precision == "fp32" else _lib.lib.prng_range_transform_f64
-
-
-def burn_once(engine: EngineKind, spec, api_mode: str, batch: int, seed: int, device: str = "cuda:0",
-              _streams=None) -> Tuple[int, object]:
+def burn_once(engine: EngineKind, spec, api_mode: str, backend: Backend, batch: int, seed: int,
+              device: str = "cuda:0") -> Tuple[int, object]:
     """One timed full cycle on the GPU; returns (tts_ns, host numpy array).  rngburn.py:111-151."""
     torch = _torch()
     if api_mode not in API_MODES:
@@ -105,51 +100,49 @@ def burn_once(engine: EngineKind, spec, api_mode: str, batch: int, seed: int, de
     if not isinstance(spec, (Uniform, Gaussian)):
         raise InvalidParameter("the burner runs uniform or gaussian requests")
     lo, hi = _transform_range(spec)
+    precision = spec.precision
     dev = torch.device(device)
-    s0 = torch.cuda.current_stream(dev)
     t0 = time.perf_counter_ns()
     state = seed_engine(engine, seed)
-    buf = torch.empty(batch, dtype=torch.float32 if spec.precision == "fp32" else torch.float64, device=dev)
     if api_mode == "hostdirect":
+        s0 = torch.cuda.current_stream(dev)
+        buf = torch.empty(batch, dtype=torch.float32 if precision == "fp32" else torch.float64, device=dev)
         generate(spec, state, batch, out=buf, stream=s0)
         if isinstance(spec, Gaussian):  # identity transform, as the reference applies it
-            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(s0)))
+            fn = _lib.lib.prng_range_transform_f32 if precision == "fp32" else _lib.lib.prng_range_transform_f64
+            _lib.check(fn(buf.data_ptr(), batch, lo, hi, _stream_handle(s0)))
+        host = buf.cpu().numpy()
     else:
-        unit = Uniform(0.0, 1.0, spec.precision) if isinstance(spec, Uniform) else spec
+        graph = TaskGraph(arena_bytes=max(2 * 1024 ** 3, 8 * batch), device=dev)
+        buf = graph.create_buffer(batch, "f32" if precision == "fp32" else "f64")
+        if isinstance(spec, Uniform):
+            gen = uniform_generate_kernel(state, buf.id, precision)
+        else:
+            gen = gaussian_generate_kernel(state, buf.id, spec.mean, spec.stddev, precision, spec.method)
+        tr = affine_kernel(buf.id, lo, hi)
         if api_mode == "buffer":
-            generate(unit, state, batch, out=buf, stream=s0)
-            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(s0)))
-        else:  # usm: producer / consumer streams joined by an explicit event
-            sa, sb = _streams if _streams is not None else (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-            sa.wait_stream(s0)
-            generate(unit, state, batch, out=buf, stream=sa)
-            ev = torch.cuda.Event()
-            ev.record(sa)
-            sb.wait_event(ev)
-            _lib.check(_range_fn(spec.precision)(buf.data_ptr(), batch, lo, hi, _stream_handle(sb)))
-            s0.wait_stream(sb)
-            buf.record_stream(sa)
-            buf.record_stream(sb)
-    host = buf.cpu().numpy()  # D2H on s0 (synchronous)
+            graph.submit_with_accessors(gen, [(buf, AccessMode.READ_WRITE)])
+            graph.submit_with_accessors(tr, [(buf, AccessMode.READ_WRITE)])
+        else:  # usm
+            e1 = graph.submit_with_events(gen, [buf], deps=[])
+            graph.submit_with_events(tr, [buf], deps=[e1])
+        graph.run(backend)
+        host = graph.copy_to_host(buf)
     tts = time.perf_counter_ns() - t0
     return tts, host
 
 
 def run_burner(config: BurnConfig) -> List[RunRecord]:
     """rngburn.py:154-177: every batch size, `iterations` cycles each."""
-    torch = _torch()
-    dev = torch.device(config.device)
-    streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    backend = f"cuda:{torch.cuda.get_device_properties(dev).multi_processor_count}sm"
     records = []
     for batch in config.batches:
         samples = []
         for _ in range(config.iterations):
-            tts, _ = burn_once(config.engine, config.dist, config.api_mode, batch, config.seed, config.device,
-                               streams)
+            tts, _ = burn_once(config.engine, config.dist, config.api_mode, config.backend, batch, config.seed,
+                               config.device)
             samples.append(tts)
-        records.append(RunRecord(config.platform, config.api_mode, backend, config.engine.value,
-                                 dist_label(config.dist), batch, samples))
+        records.append(RunRecord(config.platform, config.api_mode, backend_label(config.backend),
+                                 config.engine.value, dist_label(config.dist), batch, samples))
     if config.out_path:
         write_records_csv(records, config.out_path)
     return records

@@ -5,6 +5,7 @@ import pytest
 
 import paper_2109_01329_b200 as P
 from paper_2109_01329_b200 import burner as B
+from paper_2109_01329_b200 import execution as X
 
 
 def test_csv_is_byte_identical_to_reference_writer(golden, tmp_path):
@@ -25,10 +26,11 @@ def test_csv_schema_mismatch(tmp_path):
 
 
 def test_config_validation_matches_reference():
-    good = dict(engine=P.EngineKind.PHILOX4X32X10, dist=P.Uniform(0.0, 1.0), api_mode="buffer", batches=[1])
+    good = dict(engine=P.EngineKind.PHILOX4X32X10, dist=P.Uniform(0.0, 1.0), api_mode="buffer",
+                backend=X.Serial(), batches=[1])
     B.BurnConfig(**good)
     for bad in ({"api_mode": "cuda"}, {"batches": []}, {"batches": [0]}, {"iterations": 0}):
-        with pytest.raises(B.ConfigError):
+        with pytest.raises(X.ConfigError):
             B.BurnConfig(**{**good, **bad})
     assert B.dist_label(P.Uniform(-1.0, 1.0)) == "uniform:-1:1"
     assert B.dist_label(P.Gaussian(2.0, 0.5)) == "gaussian:2:0.5"
@@ -46,15 +48,17 @@ def test_modes_are_bit_identical_and_match_reference_burn_once(golden_arrays, tm
         (PH, P.Uniform(-1.0, 1.0, "fp64"), 777, 13, "philox_uniform_f64_m1p1_777"),
         (PH, P.Gaussian(2.0, 0.5, method="accurate"), 1001, 7, "philox_gauss_2_0.5_1001"),
     ):
-        outs = [B.burn_once(eng, spec, mode, batch, seed)[1] for mode in B.API_MODES]
-        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2]), label
+        outs = [B.burn_once(eng, spec, mode, backend, batch, seed)[1] for mode in B.API_MODES
+                for backend in (X.Serial(), X.Parallel(4, chunk=97), X.Graph(3, chunk=250))]
+        assert all(np.array_equal(outs[0], o) for o in outs[1:]), label
         want = golden_arrays[f"burn__{label}"]
         if isinstance(spec, P.Uniform):
             assert np.array_equal(outs[0], want), label
         else:  # accurate fp32 gaussian: fp64 math then one cast
             assert np.max(np.abs(outs[0].astype(np.float64) - want)) <= np.max(np.spacing(np.abs(want)))
-    cfg = B.BurnConfig(PH, P.Uniform(-1.0, 1.0), "usm", [10, 1000], iterations=3, seed=1,
+    cfg = B.BurnConfig(PH, P.Uniform(-1.0, 1.0), "usm", X.Parallel(2), [10, 1000], iterations=3, seed=1,
                        out_path=str(tmp_path / "g.csv"))
     recs = B.run_burner(cfg)
     assert [r.batch for r in recs] == [10, 1000] and all(t > 0 for r in recs for t in r.samples)
+    assert recs[0].backend == "parallel:2"
     assert len(B.read_rows_csv(str(tmp_path / "g.csv"))) == 6
