@@ -310,7 +310,9 @@ def run_c5_full(args):
                                                        "segment launch, deposition kernels and D2H of results"},
         "e2e": {"value": nev / sec, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(res["cells"].nbytes + res["energy"].nbytes)},
-        "cpu_baseline": cpu, "gpu_launches": 5,
+        # per step: control-word segments, batch segments, hits, normalise, 3 radix
+        # passes (cell_bits = 18), count, 2 scan kernels, write (profiles/r1_launches_bench_c5_full.csv)
+        "cpu_baseline": cpu, "gpu_launches": 11,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -224,22 +224,11 @@ __device__ __forceinline__ void mat3_apply(const uint32_t* J, uint32_t& a, uint3
 
 // ---------------------------------------------------------- transforms
 // Word -> unit: (w >> 8) * 2^-24, exact in fp32 and fp64 (distributions.py:78-87).
-//
-// Without I2FP (which issues on the FMA-heavy pipe, already saturated by the
-// Philox IMAD.WIDEs): one funnel shift puts m = w >> 8 under the exponent
-// of 0.5, F = bits(0x3F000000 | m).  The top bit of m lands on the exponent's
-// LSB, so F = 0.5 + u when u < 0.5 and F = 2u when u >= 0.5 (u = m 2^-24),
-// and u = min(F - 0.5, F * 0.5): both candidates are exact and the smaller
-// is always the right one (exhaustively checked over all 2^24 m,
-// tools/check_unit_trick.c).
-#ifndef PRNG_UNIT_I2FP
-__device__ __forceinline__ float unit_f32(uint32_t w) {
-    const float f = __uint_as_float(__funnelshift_r(w, 0x3Fu, 8));
-    return fminf(__fadd_rn(f, -0.5f), __fmul_rn(f, 0.5f));
-}
-#else
+// I2FP + FMUL.  (An I2FP-free exact alternative -- F = bits(0x3F000000 |
+// (w >> 8)), u = min(F - 0.5, F * 0.5), tools/check_unit_trick.c -- moves the
+// conversion off the FMA-heavy pipe but measured 0.4-1.4% slower on B200:
+// the extra ALU/FMA-lite instructions cost more than the I2FP.)
 __device__ __forceinline__ float unit_f32(uint32_t w) { return __fmul_rn((float)(w >> 8), kUnitF); }
-#endif
 // 2^52 + (w >> 8) built from bits (no I2F.F64 on the XU pipe): the 24-bit
 // integer sits in the low mantissa bits of 2^52.
 __device__ __forceinline__ double u24_magic(uint32_t w) { return __hiloint2double(0x43300000, (int)(w >> 8)); }

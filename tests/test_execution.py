@@ -131,7 +131,7 @@ def test_pending_writes_and_backend_parsing():
 
 torch = pytest.importorskip("torch")
 gpu = pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
-BACKENDS = (X.Serial(), X.Parallel(2, chunk=97), X.Parallel(4), X.Graph(3, chunk=33), X.Graph(8))
+BACKENDS = (X.Serial(), X.Parallel(2, chunk=9973), X.Parallel(4), X.Graph(3, chunk=3331), X.Graph(8))
 
 
 @pytest.mark.gpu
