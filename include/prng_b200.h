@@ -51,6 +51,12 @@ extern "C" {
  * fp64 formula, then cast (fp64 outputs always use ACCURATE). */
 #define PRNG_METHOD_FAST 0
 #define PRNG_METHOD_ACCURATE 1
+/* Gaussian only (fp32 and fp64): bit-identical to the reference's fp64
+ * Box-Muller (_core.pyx:116-121 with the host libm): log(u1') and
+ * (sin t, cos t) are gathered from tables tabulated from the host libm over
+ * their whole 2^24-point domains (built once per process, 384 MB per device;
+ * prng_exact_tables_prepare builds them ahead of the first request). */
+#define PRNG_METHOD_EXACT 2
 
 int prng_abi_version(void);
 const char *prng_last_error(void);
@@ -71,6 +77,9 @@ int prng_philox4x32x10_gaussian_f32(uint32_t k0, uint32_t k1, const uint32_t ctr
                                     double mean, double stddev, int method, float *out, void *stream);
 int prng_philox4x32x10_gaussian_f64(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
                                     double mean, double stddev, double *out, void *stream);
+int prng_philox4x32x10_gaussian_f64_method(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane,
+                                           uint64_t n, double mean, double stddev, int method, double *out,
+                                           void *stream);
 /* lognormal (extension; oneMKL lognormal(m, s, displ, scale)) */
 int prng_philox4x32x10_lognormal_f32(uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n,
                                      double m, double s, double displ, double scale, int method, float *out,
@@ -90,6 +99,8 @@ int prng_mrg32k3a_gaussian_f32(const uint32_t s1[3], const uint32_t s2[3], uint6
                                double stddev, int method, float *out, void *stream);
 int prng_mrg32k3a_gaussian_f64(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double mean,
                                double stddev, double *out, void *stream);
+int prng_mrg32k3a_gaussian_f64_method(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double mean,
+                                      double stddev, int method, double *out, void *stream);
 int prng_mrg32k3a_lognormal_f32(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double m, double s,
                                 double displ, double scale, int method, float *out, void *stream);
 int prng_mrg32k3a_lognormal_f64(const uint32_t s1[3], const uint32_t s2[3], uint64_t n, double m, double s,
@@ -113,6 +124,15 @@ int prng_gaussian_from_words_f32(const uint32_t *words, uint64_t n, double mean,
                                  float *out, void *stream);
 int prng_gaussian_from_words_f64(const uint32_t *words, uint64_t n, double mean, double stddev, double *out,
                                  void *stream);
+int prng_gaussian_from_words_f64_method(const uint32_t *words, uint64_t n, double mean, double stddev, int method,
+                                        double *out, void *stream);
+
+/* Exact-method tables: build (host libm) and upload for the current device
+ * now instead of at the first PRNG_METHOD_EXACT request; and the host copies
+ * (2^24 doubles log(m 2^-24), m = 1..2^24; 2^24 (sin, cos) pairs of
+ * fl(TWO_PI k 2^-24)) for inspection. */
+int prng_exact_tables_prepare(void);
+int prng_exact_tables_host(const double **log_table, const double **sincos_table);
 
 /* ---- Many small batches (FastCaloSim consumer, calosim.py:269-358). ----
  * One launch generates every segment: segment i writes `count` fp32 uniforms

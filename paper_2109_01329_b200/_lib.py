@@ -27,6 +27,7 @@ PRNG_ERR_CUDA = -5
 
 METHOD_FAST = 0
 METHOD_ACCURATE = 1
+METHOD_EXACT = 2
 
 _u32 = ctypes.c_uint32
 _u64 = ctypes.c_uint64
@@ -46,6 +47,7 @@ SIGNATURES = {
     "prng_philox4x32x10_uniform_f64": (_P + [_dbl, _dbl, _vp, _vp], _int),
     "prng_philox4x32x10_gaussian_f32": (_P + [_dbl, _dbl, _int, _vp, _vp], _int),
     "prng_philox4x32x10_gaussian_f64": (_P + [_dbl, _dbl, _vp, _vp], _int),
+    "prng_philox4x32x10_gaussian_f64_method": (_P + [_dbl, _dbl, _int, _vp, _vp], _int),
     "prng_philox4x32x10_lognormal_f32": (_P + [_dbl, _dbl, _dbl, _dbl, _int, _vp, _vp], _int),
     "prng_philox4x32x10_lognormal_f64": (_P + [_dbl, _dbl, _dbl, _dbl, _vp, _vp], _int),
     "prng_mrg32k3a_bits": (_M + [_vp, _vp], _int),
@@ -53,6 +55,7 @@ SIGNATURES = {
     "prng_mrg32k3a_uniform_f64": (_M + [_dbl, _dbl, _vp, _vp], _int),
     "prng_mrg32k3a_gaussian_f32": (_M + [_dbl, _dbl, _int, _vp, _vp], _int),
     "prng_mrg32k3a_gaussian_f64": (_M + [_dbl, _dbl, _vp, _vp], _int),
+    "prng_mrg32k3a_gaussian_f64_method": (_M + [_dbl, _dbl, _int, _vp, _vp], _int),
     "prng_mrg32k3a_lognormal_f32": (_M + [_dbl, _dbl, _dbl, _dbl, _int, _vp, _vp], _int),
     "prng_mrg32k3a_lognormal_f64": (_M + [_dbl, _dbl, _dbl, _dbl, _vp, _vp], _int),
     "prng_mrg32k3a_skip_ahead": ([_u32p, _u32p, _u64, _u64, _u32p, _u32p], _int),
@@ -62,6 +65,9 @@ SIGNATURES = {
     "prng_words_to_unit_f64": ([_vp, _u64, _vp, _vp], _int),
     "prng_gaussian_from_words_f32": ([_vp, _u64, _dbl, _dbl, _int, _vp, _vp], _int),
     "prng_gaussian_from_words_f64": ([_vp, _u64, _dbl, _dbl, _vp, _vp], _int),
+    "prng_gaussian_from_words_f64_method": ([_vp, _u64, _dbl, _dbl, _int, _vp, _vp], _int),
+    "prng_exact_tables_prepare": ([], _int),
+    "prng_exact_tables_host": ([ctypes.POINTER(ctypes.POINTER(ctypes.c_double))] * 2, _int),
     "prng_philox4x32x10_uniform_f32_segments": ([_u32, _u32, _vp, _u32, _u64, _dbl, _dbl, _vp, _vp], _int),
     "prng_calo_hits": ([_vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "prng_calo_deposit_scratch_bytes": ([_u64, _u32], ctypes.c_size_t),

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/prng_b200.h"
@@ -120,6 +121,139 @@ int check_lognormal(double m, double s, double displ, double scale) {
         return fail(PRNG_ERR_INVALID_PARAMETER,
                     "lognormal requires finite m, s > 0, finite displ, scale > 0, got (%g, %g, %g, %g)", m, s, displ,
                     scale);
+    return PRNG_OK;
+}
+
+int check_gauss_method(int method) {
+    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE && method != PRNG_METHOD_EXACT)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST, _ACCURATE or _EXACT");
+    return PRNG_OK;
+}
+
+// ---- exact Box-Muller tables (box_muller_exact, common.cuh) ----
+// Built once per process from the host libm -- the library the reference's
+// compiled core calls (_core.pyx:116-121) -- on every host thread, then
+// uploaded once per device.
+constexpr size_t kExactN = size_t(1) << 24;
+std::mutex g_exact_mu;
+std::vector<double> g_exact_log;
+std::vector<double2> g_exact_sc;
+
+void build_exact_host_tables() {
+    g_exact_log.resize(kExactN);
+    g_exact_sc.resize(kExactN);
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt < 1 ? 1 : (nt > 64 ? 64 : nt);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        th.emplace_back([t, nt] {
+            const double two_pi = kTwoPi;  // distributions.py:25 / _core.pyx:17
+            for (size_t i = t; i < kExactN; i += nt) {
+                volatile double u1p = (double)(i + 1) * 0x1p-24;  // 1 - u1, exact (m = i + 1)
+                g_exact_log[i] = std::log((double)u1p);
+                volatile double tt = two_pi * ((double)i * 0x1p-24);  // TWO_PI * u2, one rounding
+                const double tv = tt;
+                g_exact_sc[i] = make_double2(std::sin(tv), std::cos(tv));
+            }
+        });
+    }
+    for (auto& x : th) x.join();
+}
+
+__global__ void exact_approx_kernel(double* L, double* S, double* C) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (uint32_t)kExactN; i += gridDim.x * blockDim.x) {
+        L[i] = log_u1_f64((16777215u - i) << 8);  // m - 1 = i
+        double sn, cs;
+        sincos_ref_f64(i << 8, sn, cs);  // k = i
+        S[i] = sn;
+        C[i] = cs;
+    }
+}
+
+struct ExactDevice {
+    ExactCorrections corr{};
+    size_t escapes = 0;
+};
+std::map<int, ExactDevice> g_exact_corr;
+
+// Correction of one approximation: 4-bit ulp delta, or 8 (= -8) for an escape.
+inline uint8_t nibble(double want, double approx) {
+    long long kw, ka;
+    memcpy(&kw, &want, 8);
+    memcpy(&ka, &approx, 8);
+    const long long d = dkey(kw) - dkey(ka);
+    if (d >= -7 && d <= 7 && dunkey(dkey(ka) + d) == kw) return (uint8_t)(d & 0xF);
+    return 8;
+}
+
+int exact_tables(XformParams& p) {
+    int dev = 0;
+    PRNG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_exact_mu);
+    auto it = g_exact_corr.find(dev);
+    if (it == g_exact_corr.end()) {
+        if (g_exact_log.empty()) build_exact_host_tables();
+        // 1. the device approximations over both whole domains
+        double *dL = nullptr, *dS = nullptr, *dC = nullptr;
+        PRNG_CUDA(cudaMalloc(&dL, 3 * kExactN * sizeof(double)));
+        dS = dL + kExactN;
+        dC = dS + kExactN;
+        exact_approx_kernel<<<1184, 256>>>(dL, dS, dC);
+        std::vector<double> aL(kExactN), aS(kExactN), aC(kExactN);
+        cudaError_t e = cudaMemcpy(aL.data(), dL, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(aS.data(), dS, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemcpy(aC.data(), dC, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
+        cudaFree(dL);
+        if (e != cudaSuccess) return cuda_fail(e, "exact tables: approximations");
+        // 2. ulp corrections to the host libm, escapes where they do not fit
+        std::vector<uint8_t> lnib(kExactN / 2), scnib(kExactN);
+        for (size_t i = 0; i < kExactN; i += 2)
+            lnib[i / 2] = (uint8_t)(nibble(g_exact_log[i], aL[i]) | (nibble(g_exact_log[i + 1], aL[i + 1]) << 4));
+        for (size_t i = 0; i < kExactN; ++i)
+            scnib[i] = (uint8_t)(nibble(g_exact_sc[i].x, aS[i]) | (nibble(g_exact_sc[i].y, aC[i]) << 4));
+        std::vector<uint32_t> eidx[3];
+        std::vector<double> eval[3];
+        for (size_t i = 0; i < kExactN; ++i) {
+            if (((lnib[i / 2] >> ((i & 1) * 4)) & 0xF) == 8) {
+                eidx[0].push_back((uint32_t)i);
+                eval[0].push_back(g_exact_log[i]);
+            }
+            if ((scnib[i] & 0xF) == 8) {
+                eidx[1].push_back((uint32_t)i);
+                eval[1].push_back(g_exact_sc[i].x);
+            }
+            if ((scnib[i] >> 4) == 8) {
+                eidx[2].push_back((uint32_t)i);
+                eval[2].push_back(g_exact_sc[i].y);
+            }
+        }
+        // 3. upload: one allocation (nibbles, then each escape list)
+        size_t bytes = lnib.size() + scnib.size();
+        for (int t = 0; t < 3; ++t) bytes += eidx[t].size() * 12 + 16;
+        char* base = nullptr;
+        PRNG_CUDA(cudaMalloc(&base, bytes));
+        ExactDevice ed;
+        char* q = base;
+        PRNG_CUDA(cudaMemcpy(q, lnib.data(), lnib.size(), cudaMemcpyHostToDevice));
+        ed.corr.log_nib = reinterpret_cast<const uint8_t*>(q);
+        q += lnib.size();
+        PRNG_CUDA(cudaMemcpy(q, scnib.data(), scnib.size(), cudaMemcpyHostToDevice));
+        ed.corr.sc_nib = reinterpret_cast<const uint8_t*>(q);
+        q += scnib.size();
+        for (int t = 0; t < 3; ++t) {
+            const size_t ne = eidx[t].size();
+            PRNG_CUDA(cudaMemcpy(q, eval[t].data(), ne * 8, cudaMemcpyHostToDevice));
+            ed.corr.esc_val[t] = reinterpret_cast<const double*>(q);
+            q += ne * 8 + 8;
+            PRNG_CUDA(cudaMemcpy(q, eidx[t].data(), ne * 4, cudaMemcpyHostToDevice));
+            ed.corr.esc_idx[t] = reinterpret_cast<const uint32_t*>(q);
+            q += (ne * 4 + 8) / 8 * 8;
+            ed.corr.esc_n[t] = (uint32_t)ne;
+            ed.escapes += ne;
+        }
+        it = g_exact_corr.emplace(dev, ed).first;
+    }
+    p.exact = it->second.corr;
     return PRNG_OK;
 }
 
@@ -433,11 +567,23 @@ __global__ void range_kernel(T* v, uint64_t n, T scale, T off) {
     }
 }
 
-__global__ void box_muller_kernel(const double* u1, const double* u2, uint64_t m, double* z0, double* z1) {
+__global__ void box_muller_kernel(const double* u1, const double* u2, uint64_t m, double* z0, double* z1,
+                                  XformParams p) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-        // _core.pyx:116-121 (u1 pre-flipped by the caller)
-        const double r = sqrt(__dmul_rn(-2.0, log(u1[i])));
-        const double t = __dmul_rn(kTwoPi, u2[i]);
+        // _core.pyx:116-121 (u1 pre-flipped by the caller).  Inputs on the
+        // reference's 24-bit grid (every call the reference makes: u1' =
+        // m 2^-24, u2 = k 2^-24) take the exact route -- bit-identical to
+        // _core -- anything else the libdevice formula.
+        const double a = u1[i], b = u2[i];
+        const double ma = __dmul_rn(a, 16777216.0), kb = __dmul_rn(b, 16777216.0);
+        if (p.exact.log_nib && ma >= 1.0 && ma <= 16777216.0 && kb >= 0.0 && kb < 16777216.0 && ma == rint(ma) &&
+            kb == rint(kb)) {
+            const uint32_t w0 = (16777216u - (uint32_t)ma) << 8, w1 = (uint32_t)kb << 8;
+            box_muller_exact(w0, w1, p, z0[i], z1[i]);
+            continue;
+        }
+        const double r = sqrt(__dmul_rn(-2.0, log(a)));
+        const double t = __dmul_rn(kTwoPi, b);
         double s, c;
         sincos(t, &s, &c);
         z0[i] = __dmul_rn(r, c);
@@ -558,16 +704,39 @@ int prng_philox4x32x10_uniform_f64(PHILOX_ARGS, double a, double b, double* out,
 int prng_philox4x32x10_gaussian_f32(PHILOX_ARGS, double mean, double stddev, int method, float* out,
                                     void* stream) {
     int rc = check_gaussian(mean, stddev);
-    if (!rc) rc = check_method(method);
+    if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
-    const XformParams p = gauss_params(mean, stddev);
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        void* d = nullptr;
+        if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+        if ((rc = bind_output(out, &d)) || (rc = exact_tables(p))) return rc;
+        return launch_philox<kGaussF32Exact>(k0, k1, ctr, lane, n, out, p, stream);
+    }
     return method == PRNG_METHOD_FAST ? launch_philox<kGaussF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
                                       : launch_philox<kGaussF32Accurate>(k0, k1, ctr, lane, n, out, p, stream);
 }
 
 int prng_philox4x32x10_gaussian_f64(PHILOX_ARGS, double mean, double stddev, double* out, void* stream) {
+    return prng_philox4x32x10_gaussian_f64_method(k0, k1, ctr, lane, n, mean, stddev, PRNG_METHOD_ACCURATE, out,
+                                                  stream);
+}
+
+int prng_philox4x32x10_gaussian_f64_method(PHILOX_ARGS, double mean, double stddev, int method, double* out,
+                                           void* stream) {
     int rc = check_gaussian(mean, stddev);
-    return rc ? rc : launch_philox<kGaussF64>(k0, k1, ctr, lane, n, out, gauss_params(mean, stddev), stream);
+    if (!rc) rc = check_gauss_method(method);
+    if (rc) return rc;
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        void* d = nullptr;
+        if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+        if ((rc = bind_output(out, &d)) || (rc = exact_tables(p))) return rc;
+        return launch_philox<kGaussF64Exact>(k0, k1, ctr, lane, n, out, p, stream);
+    }
+    return launch_philox<kGaussF64>(k0, k1, ctr, lane, n, out, p, stream);  // FAST == ACCURATE for fp64
 }
 
 int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double displ, double scale, int method,
@@ -613,16 +782,38 @@ int prng_mrg32k3a_uniform_f64(MRG_ARGS, double a, double b, double* out, void* s
 
 int prng_mrg32k3a_gaussian_f32(MRG_ARGS, double mean, double stddev, int method, float* out, void* stream) {
     int rc = check_gaussian(mean, stddev);
-    if (!rc) rc = check_method(method);
+    if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
-    const XformParams p = gauss_params(mean, stddev);
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        void* d = nullptr;
+        if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+        if ((rc = bind_output(out, &d)) || (rc = exact_tables(p))) return rc;
+        return launch_mrg<kGaussF32Exact>(s1, s2, n, out, p, stream);
+    }
     return method == PRNG_METHOD_FAST ? launch_mrg<kGaussF32Fast>(s1, s2, n, out, p, stream)
                                       : launch_mrg<kGaussF32Accurate>(s1, s2, n, out, p, stream);
 }
 
 int prng_mrg32k3a_gaussian_f64(MRG_ARGS, double mean, double stddev, double* out, void* stream) {
+    return prng_mrg32k3a_gaussian_f64_method(s1, s2, n, mean, stddev, PRNG_METHOD_ACCURATE, out, stream);
+}
+
+int prng_mrg32k3a_gaussian_f64_method(MRG_ARGS, double mean, double stddev, int method, double* out,
+                                      void* stream) {
     int rc = check_gaussian(mean, stddev);
-    return rc ? rc : launch_mrg<kGaussF64>(s1, s2, n, out, gauss_params(mean, stddev), stream);
+    if (!rc) rc = check_gauss_method(method);
+    if (rc) return rc;
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        void* d = nullptr;
+        if (out == nullptr) return fail(PRNG_ERR_INVALID_PARAMETER, "out must not be NULL");
+        if ((rc = bind_output(out, &d)) || (rc = exact_tables(p))) return rc;
+        return launch_mrg<kGaussF64Exact>(s1, s2, n, out, p, stream);
+    }
+    return launch_mrg<kGaussF64>(s1, s2, n, out, p, stream);
 }
 
 int prng_mrg32k3a_lognormal_f32(MRG_ARGS, double m, double s, double displ, double scale, int method, float* out,
@@ -674,17 +865,49 @@ int prng_words_to_unit_f64(const uint32_t* words, uint64_t n, double* out, void*
 int prng_gaussian_from_words_f32(const uint32_t* words, uint64_t n, double mean, double stddev, int method,
                                  float* out, void* stream) {
     int rc = check_gaussian(mean, stddev);
-    if (!rc) rc = check_method(method);
+    if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
-    const XformParams p = gauss_params(mean, stddev);
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        if ((rc = exact_tables(p))) return rc;
+        return launch_words<kGaussF32Exact>(words, n, p, out, stream);
+    }
     return method == PRNG_METHOD_FAST ? launch_words<kGaussF32Fast>(words, n, p, out, stream)
                                       : launch_words<kGaussF32Accurate>(words, n, p, out, stream);
 }
 
 int prng_gaussian_from_words_f64(const uint32_t* words, uint64_t n, double mean, double stddev, double* out,
                                  void* stream) {
+    return prng_gaussian_from_words_f64_method(words, n, mean, stddev, PRNG_METHOD_ACCURATE, out, stream);
+}
+
+int prng_gaussian_from_words_f64_method(const uint32_t* words, uint64_t n, double mean, double stddev, int method,
+                                        double* out, void* stream) {
     int rc = check_gaussian(mean, stddev);
-    return rc ? rc : launch_words<kGaussF64>(words, n, gauss_params(mean, stddev), out, stream);
+    if (!rc) rc = check_gauss_method(method);
+    if (rc) return rc;
+    XformParams p = gauss_params(mean, stddev);
+    if (method == PRNG_METHOD_EXACT) {
+        if (n == 0) return PRNG_OK;
+        if ((rc = exact_tables(p))) return rc;
+        return launch_words<kGaussF64Exact>(words, n, p, out, stream);
+    }
+    return launch_words<kGaussF64>(words, n, p, out, stream);
+}
+
+int prng_exact_tables_prepare(void) {
+    XformParams p{};
+    return exact_tables(p);
+}
+
+int prng_exact_tables_host(const double** log_table, const double** sincos_table) {
+    if (!log_table || !sincos_table) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
+    std::lock_guard<std::mutex> lk(g_exact_mu);
+    if (g_exact_log.empty()) build_exact_host_tables();
+    *log_table = g_exact_log.data();
+    *sincos_table = reinterpret_cast<const double*>(g_exact_sc.data());
+    return PRNG_OK;
 }
 
 int prng_range_transform_f32(float* values, uint64_t n, double lo, double hi, void* stream) {
@@ -802,7 +1025,9 @@ int prng_kernels_box_muller(const double* u1, const double* u2, uint64_t m, doub
     PRNG_CUDA(cudaMemcpyAsync(du2, u2, m * 8, cudaMemcpyHostToDevice, s));
     uint64_t blocks = (m + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    box_muller_kernel<<<(unsigned)blocks, 256, 0, s>>>(du1, du2, m, dz0, dz1);
+    XformParams p{};
+    if ((rc = exact_tables(p))) return rc;
+    box_muller_kernel<<<(unsigned)blocks, 256, 0, s>>>(du1, du2, m, dz0, dz1, p);
     PRNG_CUDA(cudaGetLastError());
     PRNG_CUDA(cudaMemcpyAsync(z0, dz0, m * 8, cudaMemcpyDeviceToHost, s));
     PRNG_CUDA(cudaMemcpyAsync(z1, dz1, m * 8, cudaMemcpyDeviceToHost, s));

@@ -235,6 +235,16 @@ __device__ __forceinline__ double u24_magic(uint32_t w) { return __hiloint2doubl
 // (2^52 + x) * 2^-24 - 2^28 = x * 2^-24 exactly (one DFMA).
 __device__ __forceinline__ double unit_f64(uint32_t w) { return __fma_rn(u24_magic(w), kUnitD, -268435456.0); }
 
+// Exact gaussian method: per-input ulp corrections of the device
+// approximations to the host libm (box_muller_exact below).
+struct ExactCorrections {
+    const uint8_t* log_nib;  // 2^23 bytes: 4-bit ulp correction of log_u1_f64 per m (two per byte)
+    const uint8_t* sc_nib;   // 2^24 bytes: sin (low) / cos (high) 4-bit corrections per k
+    const uint32_t* esc_idx[3];  // escapes (correction -8): sorted indices ...
+    const double* esc_val[3];    // ... and the host-libm values; [0] log, [1] sin, [2] cos
+    uint32_t esc_n[3];
+};
+
 // Parameters of one fused request.  For uniform: (a, b) -> scale/offset with
 // the reference's precision rules (distributions.py:98-104 under numpy
 // NEP-50: fp32 arrays see f32(hi - lo) and f32(lo)).
@@ -244,6 +254,7 @@ struct XformParams {
     double mag_d;            // uniform fp64: -2^52 * scale_d
     double ln_scale, ln_displ;  // lognormal: scale, displ (fp64 path) ...
     float ln_scale_f, ln_displ_f;  // ... and fp32 path
+    ExactCorrections exact;     // exact gaussian: correction tables (device memory)
 };
 
 // Transform kinds (template parameter).
@@ -259,6 +270,8 @@ enum Xform : int {
     kLognF64 = 8,
     kUnitF32 = 9,   // uniform on [0, 1): the affine pass is an exact identity
     kUnitF64 = 10,
+    kGaussF32Exact = 11,  // the reference's fp64 Box-Muller bit for bit, cast once
+    kGaussF64Exact = 12,
 };
 
 template <int X> struct XformTraits;
@@ -273,6 +286,8 @@ template <> struct XformTraits<kGaussF64> { using T = double; static constexpr b
 template <> struct XformTraits<kLognF32Fast> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kLognF32Accurate> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kLognF64> { using T = double; static constexpr bool kPair = true; };
+template <> struct XformTraits<kGaussF32Exact> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kGaussF64Exact> { using T = double; static constexpr bool kPair = true; };
 
 // Single-word transforms.
 template <int X>
@@ -327,39 +342,42 @@ __constant__ double kCosC[10] = {1.0,                    -0.30842513753404244,  
                                  1.1501159127974052e-10, -3.8980731712596753e-13, 1.001886461636272e-15,
                                  -2.019653396886682e-18};
 
-__device__ __forceinline__ double neg2_ln_u1_f64(uint32_t w0) {
-    const double x = (double)(16777216u - (w0 >> 8));  // exact, in [1, 2^24]
+// log(u1'), u1' = 1 - (w0 >> 8) 2^-24 = m 2^-24 (intrinsics only: no
+// contraction freedom, so the exact method's correction tables, built by
+// running this same code, stay valid).
+__device__ __forceinline__ double log_u1_f64(uint32_t w0) {
+    const double x = __uint2double_rn(16777216u - (w0 >> 8));  // m, exact, in [1, 2^24]
     const int hi = __double2hiint(x);
     const int e = (hi - 0x3FE6A09E) >> 20;  // 0x3FE6A09E: high word of sqrt(1/2)
     const double f = __hiloint2double(hi - (e << 20), __double2loint(x));
-    const double g = f - 1.0;  // exact
-    const double d = f + 1.0;
+    const double g = __dsub_rn(f, 1.0);  // exact
+    const double d = __dadd_rn(f, 1.0);
     double rd;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(d));
     double er = __fma_rn(-d, rd, 1.0);
     rd = __fma_rn(rd, er, rd);
     er = __fma_rn(-d, rd, 1.0);
     rd = __fma_rn(rd, er, rd);
-    const double s = g * rd;
-    const double z = s * s;
+    const double s = __dmul_rn(g, rd);
+    const double z = __dmul_rn(s, s);
     double p = kAtanhC[8];
 #pragma unroll
     for (int i = 7; i >= 0; --i) p = __fma_rn(p, z, kAtanhC[i]);
-    const double lnf = __fma_rn(2.0 * s, z * p, 2.0 * s);
+    const double s2 = __dmul_rn(2.0, s);
+    const double lnf = __fma_rn(s2, __dmul_rn(z, p), s2);
     const double ee = (double)(e - 24);
-    const double lnx = __fma_rn(ee, kLn2Split[0], __fma_rn(ee, kLn2Split[1], lnf));
-    return -2.0 * lnx;
+    return __fma_rn(ee, kLn2Split[0], __fma_rn(ee, kLn2Split[1], lnf));
 }
 
 __device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, double& cs) {
     const uint32_t kk = k + (1u << 21);
     const uint32_t q = (kk >> 22) & 3u;
-    const double t = (double)((int)(kk & 0x3FFFFFu) - (1 << 21)) * 4.76837158203125e-07;  // exact
-    const double t2 = t * t;
+    const double t = __dmul_rn((double)((int)(kk & 0x3FFFFFu) - (1 << 21)), 4.76837158203125e-07);  // exact
+    const double t2 = __dmul_rn(t, t);
     double s = kSinC[8];
 #pragma unroll
     for (int i = 7; i >= 0; --i) s = __fma_rn(s, t2, kSinC[i]);
-    s = s * t;
+    s = __dmul_rn(s, t);
     double c = kCosC[9];
 #pragma unroll
     for (int i = 8; i >= 0; --i) c = __fma_rn(c, t2, kCosC[i]);
@@ -370,22 +388,54 @@ __device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, doubl
     sn = (q >> 1) ? -b : b;
 }
 
-__device__ __forceinline__ void box_muller_f64(uint32_t w0, uint32_t w1, double& z0, double& z1) {
-    const double r = sqrt(neg2_ln_u1_f64(w0));
+// (sin t, cos t) of the reference's argument t = fl(TWO_PI * u2)
+// (distributions.py:125, _core.pyx:119): t = 2 pi u2 + delta with
+// delta = fl(TWO_PI u2) - TWO_PI u2 - (2 pi - TWO_PI) u2, |delta| < 1e-15;
+// a first-order correction on the exactly reduced 2 pi k 2^-24 reproduces it
+// (and the reference's non-zero values at the quadrant points, e.g.
+// cos(fl(pi/2))).
+__device__ __forceinline__ void sincos_ref_f64(uint32_t w1, double& sn, double& cs) {
     double s, c;
     sincos_2pi_k24_f64(w1 >> 8, s, c);
-    // The reference takes cos/sin of fl(TWO_PI * u2) (distributions.py:125,
-    // _core.pyx:119), i.e. of 2 pi u2 + delta with
-    // delta = fl(TWO_PI u2) - TWO_PI u2 - (2 pi - TWO_PI) u2, |delta| < 1e-15.
-    // First-order correction reproduces that argument (and the reference's
-    // non-zero values at the exact quadrant points, e.g. cos(fl(pi/2))).
     const double u2 = unit_f64(w1);
     const double t = __dmul_rn(kTwoPi, u2);
     const double delta = __fma_rn(-2.4492935982947064e-16, u2, -__fma_rn(kTwoPi, u2, -t));
-    const double c2 = __fma_rn(-delta, s, c);
-    const double s2 = __fma_rn(delta, c, s);
-    z0 = __dmul_rn(r, c2);
-    z1 = __dmul_rn(r, s2);
+    cs = __fma_rn(-delta, s, c);
+    sn = __fma_rn(delta, c, s);
+}
+
+__device__ __forceinline__ void box_muller_f64(uint32_t w0, uint32_t w1, double& z0, double& z1) {
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log_u1_f64(w0)));
+    double s, c;
+    sincos_ref_f64(w1, s, c);
+    z0 = __dmul_rn(r, c);
+    z1 = __dmul_rn(r, s);
+}
+
+// ---- exact route: approximations above + per-input ulp corrections ----
+// Order-preserving integer key of a double (adjacent doubles differ by 1;
+// +0 and -0 both map to 0).
+__device__ __host__ __forceinline__ long long dkey(long long b) {
+    return b >= 0 ? b : -(b & 0x7FFFFFFFFFFFFFFFll);
+}
+__device__ __host__ __forceinline__ long long dunkey(long long k) {
+    return k >= 0 ? k : ((-k) | (long long)0x8000000000000000ull);
+}
+
+__device__ __noinline__ double exact_escape(const uint32_t* idx, const double* val, uint32_t n, uint32_t i) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (idx[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    return val[lo];
+}
+
+__device__ __forceinline__ int nib_delta(uint32_t v) { return (int)((v & 0xFu) ^ 8u) - 8; }
+
+__device__ __forceinline__ double corrected(double approx, int d, const ExactCorrections& x, int tab, uint32_t i) {
+    if (d == -8) return exact_escape(x.esc_idx[tab], x.esc_val[tab], x.esc_n[tab], i);
+    return __longlong_as_double(dunkey(dkey(__double_as_longlong(approx)) + d));
 }
 
 // Fast (fp32) route, specialised to the 24-bit inputs (DESIGN.md
@@ -480,6 +530,50 @@ template <> __device__ __forceinline__ void xform2<kGaussF32Fast>(uint32_t w0, u
     box_muller_f32(w0, w1, z0, z1);
     o0 = fmaf(z0, p.scale_f, p.off_f);
     o1 = fmaf(z1, p.scale_f, p.off_f);
+}
+
+// Exact route: the reference evaluates r = sqrt(-2.0 * log(u1')), t =
+// TWO_PI * u2, (r cos t, r sin t) in fp64 with the host libm (_core.pyx:
+// 116-121).  u1' = m 2^-24 (m in [1, 2^24]) and u2 = k 2^-24 (k < 2^24) take
+// only 2^24 values each, so the library runs the device approximations
+// (log_u1_f64, sincos_ref_f64: a few ulps) once over both whole domains,
+// compares them with the host libm's log/sin/cos and keeps the difference
+// in ulps as 4-bit corrections (24 MB, L2-resident; the rare larger
+// differences go to sorted escape lists).  Approximation + correction is
+// the host libm's value bit for bit; the remaining operations (exact -2x
+// scaling, IEEE sqrt, two products, the affine) are correctly rounded on
+// both sides, so every output is bit-identical to the reference's.
+__device__ __forceinline__ void box_muller_exact(uint32_t w0, uint32_t w1, const XformParams& p, double& z0,
+                                                 double& z1) {
+    const ExactCorrections& x = p.exact;
+    const uint32_t mi = 16777215u - (w0 >> 8);  // m - 1
+    const uint32_t k = w1 >> 8;
+    const uint32_t lb = __ldg(x.log_nib + (mi >> 1));
+    const uint32_t sb = __ldg(x.sc_nib + k);
+    const double L = corrected(log_u1_f64(w0), nib_delta(lb >> ((mi & 1u) * 4)), x, 0, mi);
+    double s, c;
+    sincos_ref_f64(w1, s, c);
+    s = corrected(s, nib_delta(sb), x, 1, k);
+    c = corrected(c, nib_delta(sb >> 4), x, 2, k);
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, L));
+    z0 = __dmul_rn(r, c);
+    z1 = __dmul_rn(r, s);
+}
+
+template <> __device__ __forceinline__ void xform2<kGaussF64Exact>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                  double& o0, double& o1) {
+    double z0, z1;
+    box_muller_exact(w0, w1, p, z0, z1);
+    o0 = __dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);  // z *= stddev; z += mean (distributions.py:128-129)
+    o1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
+}
+
+template <> __device__ __forceinline__ void xform2<kGaussF32Exact>(uint32_t w0, uint32_t w1, const XformParams& p,
+                                                                  float& o0, float& o1) {
+    double a, b;
+    xform2<kGaussF64Exact>(w0, w1, p, a, b);
+    o0 = (float)a;  // .astype(float32) (distributions.py:131)
+    o1 = (float)b;
 }
 
 // Lognormal (extension a18): x = exp(m + s*z) * scale + displ.

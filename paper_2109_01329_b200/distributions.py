@@ -15,7 +15,10 @@ Results vs the reference:
   * gaussian/lognormal fp64, and fp32 with method="accurate": fp64 math on
     the device (CUDA libdevice log/sincos/exp vs glibc), a few fp64 ulps;
   * gaussian/lognormal fp32 with method="fast" (default): fp32 logf /
-    sqrtf / sincospif / expf, within the stated fp32 tolerance.
+    sqrtf / sincospif / expf, within the stated fp32 tolerance;
+  * gaussian fp32/fp64 with method="exact": bit-identical to the reference
+    (log / sin / cos gathered from tables of the host libm over their whole
+    2^24-point input domains, csrc/common.cuh box_muller_exact).
 """
 
 from __future__ import annotations
@@ -45,7 +48,7 @@ from .errors import InvalidParameter, InvalidRange, UnsupportedEngine
 
 _UNIT_SCALE = 2.0 ** -24
 _PRECISIONS = ("fp32", "fp64")
-_METHODS = {"fast": _lib.METHOD_FAST, "accurate": _lib.METHOD_ACCURATE}
+_METHODS = {"fast": _lib.METHOD_FAST, "accurate": _lib.METHOD_ACCURATE, "exact": _lib.METHOD_EXACT}
 
 
 def _check_precision(precision: str) -> None:
@@ -53,9 +56,10 @@ def _check_precision(precision: str) -> None:
         raise InvalidParameter(f"precision must be fp32 or fp64, got {precision!r}")
 
 
-def _check_method(method: str) -> None:
-    if method not in _METHODS:
-        raise InvalidParameter(f"method must be 'fast' or 'accurate', got {method!r}")
+def _check_method(method: str, exact_ok: bool = True) -> None:
+    if method not in _METHODS or (method == "exact" and not exact_ok):
+        allowed = "'fast', 'accurate' or 'exact'" if exact_ok else "'fast' or 'accurate'"
+        raise InvalidParameter(f"method must be {allowed}, got {method!r}")
 
 
 def _dtype(precision: str):
@@ -110,7 +114,7 @@ class Lognormal:
         if not all(math.isfinite(v) for v in vals) or self.s <= 0 or self.scale <= 0:
             raise InvalidParameter(f"lognormal requires finite m, s > 0, finite displ, scale > 0, got {vals}")
         _check_precision(self.precision)
-        _check_method(self.method)
+        _check_method(self.method, exact_ok=False)
 
 
 @dataclass(frozen=True)
@@ -165,7 +169,8 @@ def gaussian_from_words(words, mean: float, stddev: float, n: int, precision: st
         rc = _lib.lib.prng_gaussian_from_words_f32(words.data_ptr(), n, mean, stddev, _METHODS[method],
                                                    out.data_ptr(), s)
     else:
-        rc = _lib.lib.prng_gaussian_from_words_f64(words.data_ptr(), n, mean, stddev, out.data_ptr(), s)
+        rc = _lib.lib.prng_gaussian_from_words_f64_method(words.data_ptr(), n, mean, stddev, _METHODS[method],
+                                                          out.data_ptr(), s)
     _lib.check(rc)
     return out[:n]
 
@@ -184,7 +189,7 @@ def _entry(kind: EngineKind, spec: DistributionSpec):
         if spec.precision == "fp32":
             name, tail = "gaussian_f32", (spec.mean, spec.stddev, _METHODS[spec.method])
         else:
-            name, tail = "gaussian_f64", (spec.mean, spec.stddev)
+            name, tail = "gaussian_f64_method", (spec.mean, spec.stddev, _METHODS[spec.method])
     elif isinstance(spec, Lognormal):
         if spec.precision == "fp32":
             name, tail = "lognormal_f32", (spec.m, spec.s, spec.displ, spec.scale, _METHODS[spec.method])
@@ -277,3 +282,17 @@ def fill_lognormal(state: EngineState, n: int, m: float = 0.0, s: float = 1.0, d
         raise InvalidParameter("count must be non-negative")
     state, values = generate(Lognormal(m, s, displ, scale, precision, method), state, n, out, stream)
     return state, RandomBlock(values=values, count=n, precision=precision)
+
+
+def exact_tables_host():
+    """The exact method's host tables as numpy views (no copy): log(m 2^-24)
+    for m = 1..2^24, and (sin t, cos t) for t = fl(TWO_PI k 2^-24), k < 2^24."""
+    import numpy as np
+
+    lp = ctypes.POINTER(ctypes.c_double)()
+    sp = ctypes.POINTER(ctypes.c_double)()
+    _lib.check(_lib.lib.prng_exact_tables_host(ctypes.byref(lp), ctypes.byref(sp)))
+    n = 1 << 24
+    log_tab = np.ctypeslib.as_array(lp, shape=(n,))
+    sc_tab = np.ctypeslib.as_array(sp, shape=(n, 2))
+    return log_tab, sc_tab

@@ -269,7 +269,12 @@ def test_kernels_dropin_matches_reference_kernel_tests():
     u2 = rng.integers(0, 2**24, 20000).astype(np.float64) / 2**24
     c0, c1 = K.box_muller(u1, u2)
     o0, o1 = O.box_muller(u1, u2)
-    # test_kernels.py:58-67 tolerance between two libm-grade implementations
+    # on the reference's 24-bit grid the drop-in is bit-identical to _core (exact route) ...
+    assert np.array_equal(c0, o0) and np.array_equal(c1, o1)
+    # ... and off the grid within test_kernels.py:58-67's libm-to-libm tolerance
+    v1, v2 = rng.uniform(1e-300, 1.0, 5000), rng.uniform(0.0, 1.0, 5000)
+    c0, c1 = K.box_muller(v1, v2)
+    o0, o1 = O.box_muller(v1, v2)
     assert np.allclose(c0, o0, rtol=1e-13, atol=1e-13) and np.allclose(c1, o1, rtol=1e-13, atol=1e-13)
 
 

@@ -44,6 +44,8 @@ def main():
         ("philox gauss f32 fast", ph, P.Gaussian(0.0, 1.0), torch.float32, 1 << 30),
         ("philox gauss f32 acc", ph, P.Gaussian(0.0, 1.0, method="accurate"), torch.float32, 1 << 30),
         ("philox gauss f64", ph, P.Gaussian(0.0, 1.0, "fp64"), torch.float64, 1 << 29),
+        ("philox gauss f32 exact", ph, P.Gaussian(0.0, 1.0, method="exact"), torch.float32, 1 << 30),
+        ("philox gauss f64 exact", ph, P.Gaussian(0.0, 1.0, "fp64", "exact"), torch.float64, 1 << 29),
         ("philox logn f32 fast", ph, P.Lognormal(), torch.float32, 1 << 30),
         ("mrg bits", mr, P.UniformBits(), torch.uint32, 1 << 28),
         ("mrg uniform f64 [-1,1)", mr, P.Uniform(-1.0, 1.0, "fp64"), torch.float64, 1 << 28),
