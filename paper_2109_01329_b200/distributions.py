@@ -119,7 +119,16 @@ class Lognormal:
 
 @dataclass(frozen=True)
 class UniformBits:
-    """Raw 32-bit words (oneMKL uniform_bits<uint32>)."""
+    """Raw engine words: oneMKL uniform_bits<uint32> (bits=32, one word per
+    sample) or uniform_bits<uint64> (bits=64: sample i = word 2i | word
+    (2i+1) << 32, i.e. the 32-bit stream read as little-endian 64-bit
+    values; two words per sample)."""
+
+    bits: int = 32
+
+    def __post_init__(self):
+        if self.bits not in (32, 64):
+            raise InvalidParameter(f"uniform_bits width must be 32 or 64, got {self.bits!r}")
 
 
 DistributionSpec = Union[Uniform, Gaussian, Lognormal, UniformBits]
@@ -138,6 +147,8 @@ def words_consumed(spec: DistributionSpec, n: int) -> int:
     """Stream words a request of n samples consumes (distributions.py:146-149)."""
     if isinstance(spec, (Gaussian, Lognormal)):
         return 2 * ((n + 1) // 2)
+    if isinstance(spec, UniformBits) and spec.bits == 64:
+        return 2 * n
     return n
 
 
@@ -214,13 +225,14 @@ def _launch(spec: DistributionSpec, state, n: int, ptr: int, s) -> None:
     else:
         raise UnsupportedEngine(f"unknown engine state: {type(state).__name__}")
     fn, tail = _entry(kind, spec)
-    _lib.check(fn(*head, n, *tail, ptr, s))
+    # uniform_bits<uint64>: the 2n-word stream written as little-endian pairs
+    _lib.check(fn(*head, words_consumed(spec, n) if isinstance(spec, UniformBits) else n, *tail, ptr, s))
 
 
 def out_dtype(spec: DistributionSpec):
     torch = _torch()
     if isinstance(spec, UniformBits):
-        return torch.uint32
+        return torch.uint64 if spec.bits == 64 else torch.uint32
     return _dtype(spec.precision)
 
 

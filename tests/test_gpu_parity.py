@@ -468,3 +468,19 @@ def test_onemkl_engine_objects_stream_like_states():
             st, b = P.generate(spec, st, n)
             assert torch.equal(a, b)
             assert eng.state == st
+
+
+def test_uniform_bits_64_is_the_word_stream_in_little_endian_pairs():
+    """oneMKL uniform_bits<uint64>: sample i = word 2i | word 2i+1 << 32; the
+    state advances 2n words (Philox and MRG)."""
+    for kind, ost in ((P.EngineKind.PHILOX4X32X10, None), (P.EngineKind.MRG32K3A, None)):
+        st = P.skip_ahead(P.seed_engine(kind, 31), 5)
+        new, got = P.generate(P.UniformBits(64), st, 1001)
+        assert got.dtype == torch.uint64 and got.numel() == 1001
+        _, w = P.generate_words(st, 2002)
+        words = w.cpu().numpy()
+        want = words[0::2].astype(np.uint64) | (words[1::2].astype(np.uint64) << np.uint64(32))
+        assert np.array_equal(got.cpu().numpy(), want)
+        assert P.generate_words(new, 3)[1].cpu().tolist() == P.generate_words(P.skip_ahead(st, 2002), 3)[1].cpu().tolist()
+    with pytest.raises(P.InvalidParameter):
+        P.UniformBits(16)
