@@ -492,14 +492,51 @@ __device__ __forceinline__ void sincos_2pi_k24(uint32_t k, float& sn, float& cs)
     sn = __int_as_float(__float_as_int(b) ^ ((q >> 1) << 31));
 }
 
-__device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {
+#ifndef PRNG_BM_FAST_V2
+#define PRNG_BM_FAST_V2 1
+#endif
+// -2 ln u1' with one SFU op for most inputs (fewer issue slots than the
+// polynomial above; the fast gaussian is issue-bound):
+//  * u1 = k 2^-24 >= 2^-4: -2 ln2 * lg2.approx(1 - u1) (1 - u1 exact); the
+//    SFU's relative error here is <= 2^-20.5 (measured exhaustively,
+//    tools/mufu_accuracy.cu), i.e. <= 2^-21.5 in r;
+//  * u1 < 2^-4: the series -2 ln(1 - x) = x (2 + x + 2x^2/3 + ... + 2x^6/7),
+//    truncation < 2^-27 relative, so r keeps full relative accuracy as
+//    u1' -> 1.
+__device__ __forceinline__ float neg2_ln_u1_v2(uint32_t w0) {
+    const uint32_t k = w0 >> 8;
+    const float x = __uint2float_rn(k) * 5.9604644775390625e-08f;  // u1, exact
+    float p = 0.28571428571f;                                        // 2/7
+    p = fmaf(p, x, 0.33333333333f);
+    p = fmaf(p, x, 0.4f);
+    p = fmaf(p, x, 0.5f);
+    p = fmaf(p, x, 0.66666666667f);
+    p = fmaf(p, x, 1.0f);
+    p = fmaf(p, x, 2.0f);
+    float l2;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(1.0f - x));  // 1 - x >= 2^-24: normal
+    return k < (1u << 20) ? x * p : l2 * -1.3862943611198906f;
+}
+
+// (r, sin, cos) of the fast route; r = sqrt(-2 ln u1') by MUFU.SQRT
+// (relative error <= 2^-23.2, exhaustive).
+__device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, float& r, float& sn, float& cs) {
+#if PRNG_BM_FAST_V2
+    const float s2 = neg2_ln_u1_v2(w0);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s2));  // s2 = 0 or >= 1.19e-7
+#else
     const float s2 = neg2_ln_u1(w0);
     // s2 is 0 (u1' = 1) or >= 1.19e-7 (normal): the raw MUFU.RSQ (ftz) is safe.
     float rs;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(s2));
-    const float r = s2 > 0.0f ? s2 * rs : 0.0f;
-    float sn, cs;
+    r = s2 > 0.0f ? s2 * rs : 0.0f;
+#endif
     sincos_2pi_k24(w1 >> 8, sn, cs);
+}
+
+__device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {
+    float r, sn, cs;
+    box_muller_f32_parts(w0, w1, r, sn, cs);
     z0 = r * cs;
     z1 = r * sn;
 }
@@ -526,10 +563,11 @@ template <> __device__ __forceinline__ void xform2<kGaussF32Accurate>(uint32_t w
 
 template <> __device__ __forceinline__ void xform2<kGaussF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
                                                                  float& o0, float& o1) {
-    float z0, z1;
-    box_muller_f32(w0, w1, z0, z1);
-    o0 = fmaf(z0, p.scale_f, p.off_f);
-    o1 = fmaf(z1, p.scale_f, p.off_f);
+    float r, sn, cs;
+    box_muller_f32_parts(w0, w1, r, sn, cs);
+    const float rs = r * p.scale_f;  // stddev folded into r: mean + (r sd) cos t
+    o0 = fmaf(rs, cs, p.off_f);
+    o1 = fmaf(rs, sn, p.off_f);
 }
 
 // Exact route: the reference evaluates r = sqrt(-2.0 * log(u1')), t =
@@ -597,10 +635,11 @@ template <> __device__ __forceinline__ void xform2<kLognF32Accurate>(uint32_t w0
 
 template <> __device__ __forceinline__ void xform2<kLognF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
                                                                 float& o0, float& o1) {
-    float z0, z1;
-    box_muller_f32(w0, w1, z0, z1);
-    o0 = fmaf(expf(fmaf(z0, p.scale_f, p.off_f)), p.ln_scale_f, p.ln_displ_f);
-    o1 = fmaf(expf(fmaf(z1, p.scale_f, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+    float r, sn, cs;
+    box_muller_f32_parts(w0, w1, r, sn, cs);
+    const float rs = r * p.scale_f;
+    o0 = fmaf(expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+    o1 = fmaf(expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
 }
 
 // Four consecutive stream words -> four outputs.  For pair transforms the
