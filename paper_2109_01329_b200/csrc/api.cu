@@ -530,7 +530,7 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     if (rc) return rc;
     const uint64_t tmax = (uint64_t)sms * occ * kMrgThreads;
     uint64_t chunk = (n + tmax - 1) / tmax;
-    chunk = (chunk + 2 * TW - 1) / (2 * TW) * (2 * TW);  // two interleaved halves of whole tiles
+    chunk = (chunk + kMrgChains * TW - 1) / (kMrgChains * TW) * (kMrgChains * TW);  // chains x whole tiles
     const uint64_t tact = (n + chunk - 1) / chunk;
     uint32_t nbits = 0;
     while (nbits < 64 && ((tact - 1) >> nbits) != 0) ++nbits;

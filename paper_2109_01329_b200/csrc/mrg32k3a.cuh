@@ -24,6 +24,10 @@ constexpr int kMrgThreads = 128;
 #define PRNG_MRG_MINB 6
 #endif
 constexpr int kMrgMinBlocks = PRNG_MRG_MINB;
+#ifndef PRNG_MRG_CHAINS
+#define PRNG_MRG_CHAINS 2
+#endif
+constexpr int kMrgChains = PRNG_MRG_CHAINS;  // interleaved recurrences per thread (1 or 2)
 
 struct MrgLaunch {
     uint32_t s1[3], s2[3];
@@ -66,29 +70,35 @@ __device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
 
 // Write one staged tile (row j = run j, starting at run0 + j*chunk).  Each
 // instruction moves four runs' 128-byte lines: lane L handles row
-// 4i + (L >> 3), chunk L & 7.
+// 4i + (L >> 3), chunk L & 7.  The common case (tile entirely inside the
+// request, 16-byte aligned output) is a straight-line block of 8 LDS.128 +
+// 8 STG.128 with one 64-bit stride add each; the predicated element path
+// only runs for the request's last tiles.
 template <typename T>
 __device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ run0, uint64_t chunk, uint32_t lane,
                                                uint64_t first_elem, uint64_t n, bool vec_ok) {
     constexpr int CE = 16 / sizeof(T);
     constexpr int TW = 8 * CE;
-    const bool full = vec_ok && first_elem + 31 * chunk + TW <= n;  // warp-uniform
     const uint32_t x = lane & 7;
     const uint32_t r0 = lane >> 3;
     T* p = run0 + r0 * chunk + x * CE;
+    const uint64_t stride = 4 * chunk;
+    if (vec_ok && first_elem + 31 * chunk + TW <= n) {  // warp-uniform
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const uint32_t j = 4 * i + r0;
+            st_global_cs_v4(p + i * stride, st[j * 8 + (x ^ (j & 7))]);
+        }
+        return;
+    }
     uint64_t e = first_elem + r0 * chunk + x * CE;
-#pragma unroll 2
-    for (int i = 0; i < 8; ++i, p += 4 * chunk, e += 4 * chunk) {
+    for (int i = 0; i < 8; ++i, p += stride, e += stride) {
         const uint32_t j = 4 * i + r0;
         const uint4 v = st[j * 8 + (x ^ (j & 7))];
-        if (full) {
-            st_global_cs_v4(p, v);
-        } else {
-            const T* vv = reinterpret_cast<const T*>(&v);
+        const T* vv = reinterpret_cast<const T*>(&v);
 #pragma unroll
-            for (int q = 0; q < CE; ++q)
-                if (e + q < n) p[q] = vv[q];
-        }
+        for (int q = 0; q < CE; ++q)
+            if (e + q < n) p[q] = vv[q];
     }
 }
 
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
     using T = typename XformTraits<X>::T;
     constexpr int TW = MrgTile<T>::kWords;
     constexpr int WARPS = kMrgThreads / 32;
-    __shared__ uint4 stage[2][WARPS][32 * 8];
+    __shared__ uint4 stage[kMrgChains][WARPS][32 * 8];
     __shared__ uint32_t sj1[kMrgMaxBits * 9], sj2[kMrgMaxBits * 9];
 
     for (uint32_t i = threadIdx.x; i < a.nbits * 9; i += blockDim.x) {
@@ -121,15 +131,18 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
     }
     MrgStateF64 sa{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
                    mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
-    mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
-    mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
-    MrgStateF64 sb{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
-                   mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
+    MrgStateF64 sb = sa;
+    if constexpr (kMrgChains == 2) {
+        mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
+        mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
+        sb = MrgStateF64{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
+                         mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
+    }
 
-    const uint64_t half = a.chunk >> 1;
+    const uint64_t half = a.chunk / kMrgChains;
     T* __restrict__ out = static_cast<T*>(a.out);
     uint4* sta = stage[0][warp];
-    uint4* stb = stage[1][warp];
+    uint4* stb = stage[kMrgChains - 1][warp];
     const bool vec_ok = ((uintptr_t)out & 15u) == 0;
     const uint64_t warp_elem0 = t_warp0 * a.chunk;
     constexpr int CE = 16 / sizeof(T);  // elements per 16-byte chunk
@@ -142,27 +155,29 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
 #pragma unroll
                 for (int k = 0; k < CE; k += 2) {
                     const uint32_t a0 = mrg_step_f64(sa);
-                    const uint32_t b0 = mrg_step_f64(sb);
                     const uint32_t a1 = mrg_step_f64(sa);
-                    const uint32_t b1 = mrg_step_f64(sb);
                     xform2<X>(a0, a1, a.p, oa[k], oa[k + 1]);
-                    xform2<X>(b0, b1, a.p, ob[k], ob[k + 1]);
+                    if constexpr (kMrgChains == 2) {
+                        const uint32_t b0 = mrg_step_f64(sb);
+                        const uint32_t b1 = mrg_step_f64(sb);
+                        xform2<X>(b0, b1, a.p, ob[k], ob[k + 1]);
+                    }
                 }
             } else {
 #pragma unroll
                 for (int k = 0; k < CE; ++k) {
-                    const uint32_t wa = mrg_step_f64(sa);
-                    const uint32_t wb = mrg_step_f64(sb);
-                    oa[k] = xform1<X>(wa, a.p);
-                    ob[k] = xform1<X>(wb, a.p);
+                    oa[k] = xform1<X>(mrg_step_f64(sa), a.p);
+                    if constexpr (kMrgChains == 2) ob[k] = xform1<X>(mrg_step_f64(sb), a.p);
                 }
             }
             stage_put(sta, lane, c, pack16<T>(oa));
-            stage_put(stb, lane, c, pack16<T>(ob));
+            if constexpr (kMrgChains == 2) stage_put(stb, lane, c, pack16<T>(ob));
         }
         __syncwarp();
         mrg_store_tile<T>(sta, out + warp_elem0 + off, a.chunk, lane, warp_elem0 + off, a.n, vec_ok);
-        mrg_store_tile<T>(stb, out + warp_elem0 + half + off, a.chunk, lane, warp_elem0 + half + off, a.n, vec_ok);
+        if constexpr (kMrgChains == 2)
+            mrg_store_tile<T>(stb, out + warp_elem0 + half + off, a.chunk, lane, warp_elem0 + half + off, a.n,
+                              vec_ok);
         __syncwarp();
     }
 }

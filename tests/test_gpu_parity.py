@@ -484,3 +484,22 @@ def test_uniform_bits_64_is_the_word_stream_in_little_endian_pairs():
         assert P.generate_words(new, 3)[1].cpu().tolist() == P.generate_words(P.skip_ahead(st, 2002), 3)[1].cpu().tolist()
     with pytest.raises(P.InvalidParameter):
         P.UniformBits(16)
+
+
+@pytest.mark.parametrize("dist,prec", [("bits", "fp32"), ("uniform", "fp32"), ("uniform", "fp64"),
+                                       ("gaussian", "fp32"), ("gaussian", "fp64")])
+def test_body_launches_split_at_2p32_block_boundaries(dist, prec):
+    """The host cuts a request's vectorised body into launches at every
+    2^32-block boundary (upper counter words uniform per launch, philox.cuh);
+    requests straddling one (and the full 128-bit wrap) equal the oracle."""
+    key = (0x1234, 0x5678)
+    for ctr, lane in (((0xFFFFFF00, 5, 0, 0), 0), ((0xFFFFFFF7, 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFF), 3),
+                      ((0xFFFFFF03, 0xFFFFFFFF, 7, 0), 1)):
+        st = P.PhiloxState(key, ctr, lane_index=4)
+        st = P.skip_ahead(st, lane) if lane else st
+        n = (1 << 16) + 13
+        spec = spec_for(dist, prec, 0.5 if dist == "gaussian" else -2.0, 3.0, "accurate")
+        _, got = P.generate(spec, st, n)
+        want = O.generate("philox", (key, P.stream_position(st)), dist, n, prec, 0.5 if dist == "gaussian" else -2.0,
+                          3.0)
+        compare(dist, prec, host(got), want, 0.5 if dist == "gaussian" else -2.0, 3.0, "accurate", (ctr, lane))
