@@ -377,7 +377,8 @@ def test_state_round_trip_matches_reference_accounting():
     assert tuple(words) == (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)
 
 
-@pytest.mark.parametrize("prec,method", [("fp64", "accurate"), ("fp32", "fast"), ("fp32", "accurate")])
+@pytest.mark.parametrize("prec,method", [("fp64", "accurate"), ("fp32", "fast"), ("fp32", "accurate"),
+                                         ("fp64", "exact"), ("fp32", "exact")])
 def test_box_muller_exhaustive_24bit(prec, method):
     """Every one of the 2^24 possible u1 (and, separately, u2) values through
     gaussian_from_words vs the oracle's libm Box-Muller: the stated tolerance
@@ -392,6 +393,10 @@ def test_box_muller_exhaustive_24bit(prec, method):
         want = O.gaussian_from_words(words, 0.0, 1.0, 2 << 24, prec)
         got = host(P.gaussian_from_words(torch.from_numpy(words).cuda(), 0.0, 1.0, 2 << 24, prec, method))
         dt = np.float32 if prec == "fp32" else np.float64
+        if method == "exact":  # bit-identical on the whole 24-bit input domain
+            ui = np.uint32 if prec == "fp32" else np.uint64
+            assert np.array_equal(got.view(ui), want.view(ui)), f"{prec}/exact"
+            continue
         err, exact = check_close(got, want, gaussian_allowed(want, 0.0, 1.0, dt, method == "fast"),
                                  f"{prec}/{method}")
         print(f"{prec}/{method}: max abs err {err:.3e}, bit-exact fraction {exact:.6f}")
