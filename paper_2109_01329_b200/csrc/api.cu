@@ -486,7 +486,9 @@ struct MrgTables {
 std::mutex g_mrg_mu;
 std::map<std::pair<uint64_t, uint32_t>, MrgTables> g_mrg_tables;
 
-const MrgTables& mrg_tables(uint64_t chunk, uint32_t nbits) {
+// Returned by value: another thread may evict the cache entry right after
+// the lock is released.
+MrgTables mrg_tables(uint64_t chunk, uint32_t nbits) {
     std::lock_guard<std::mutex> lk(g_mrg_mu);
     auto key = std::make_pair(chunk, nbits);
     auto it = g_mrg_tables.find(key);
@@ -535,7 +537,7 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     uint32_t nbits = 0;
     while (nbits < 64 && ((tact - 1) >> nbits) != 0) ++nbits;
     if (nbits > (uint32_t)kMrgMaxBits) return fail(PRNG_ERR_INVALID_PARAMETER, "request too large");
-    const MrgTables& tb = mrg_tables(chunk, nbits);
+    const MrgTables tb = mrg_tables(chunk, nbits);
     MrgLaunch a{};
     for (int i = 0; i < 3; ++i) {
         a.s1[i] = s1[i];

@@ -508,3 +508,43 @@ def test_body_launches_split_at_2p32_block_boundaries(dist, prec):
         want = O.generate("philox", (key, P.stream_position(st)), dist, n, prec, 0.5 if dist == "gaussian" else -2.0,
                           3.0)
         compare(dist, prec, host(got), want, 0.5 if dist == "gaussian" else -2.0, 3.0, "accurate", (ctr, lane))
+
+
+def test_concurrent_host_threads_and_streams():
+    """The C ABI is called from many host threads at once (ctypes drops the
+    GIL), each on its own stream, with different request shapes (MRG table
+    cache, exact-table init, occupancy cache): every result equals the oracle."""
+    import threading
+
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            for j in range(6):
+                n = 1000 + 7919 * (i + 1) * (j + 1)
+                if (i + j) % 3 == 0:
+                    st = P.skip_ahead(P.seed_engine(MRG, 100 + i), j)
+                    _, got = P.generate(P.UniformBits(), st, n, stream=s)
+                    s1, s2 = O.mrg_skip(*O.seed_mrg(100 + i), j)
+                    want = O.mrg_fill(*s1, *s2, n)[0]
+                elif (i + j) % 3 == 1:
+                    st = P.skip_ahead(P.seed_engine(PHILOX, 100 + i), j)
+                    _, got = P.generate(P.Uniform(-1.0, 2.0), st, n, stream=s)
+                    want = O.generate("philox", (O.seed_philox(100 + i), j), "uniform", n, "fp32", -1.0, 2.0)
+                else:
+                    st = P.seed_engine(PHILOX, 100 + i)
+                    _, got = P.generate(P.Gaussian(0.0, 1.0, "fp64", "exact"), st, n, stream=s)
+                    want = O.generate("philox", (O.seed_philox(100 + i), 0), "gaussian", n, "fp64", 0.0, 1.0)
+                s.synchronize()
+                if not np.array_equal(got.cpu().numpy(), want):
+                    errors.append((i, j))
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append((i, repr(exc)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
