@@ -518,6 +518,42 @@ __device__ __forceinline__ float neg2_ln_u1_v2(uint32_t w0) {
     return k < (1u << 20) ? x * p : l2 * -1.3862943611198906f;
 }
 
+#ifndef PRNG_SINCOS_TAB
+#define PRNG_SINCOS_TAB 1
+#endif
+// Fast-route (sin, cos)(2 pi k 2^-24) by angle addition: a per-CTA
+// shared-memory table of (sin, cos)(2 pi j / 1024) (8 KB, filled by the
+// kernel prologue with sincospif) for the top 10 bits of k, and
+// sin(x) = x - x^3/6, cos(x) = 1 - x^2/2 for the remaining x < 2 pi 2^-10
+// (truncation < 6e-11).  Table rounding + combination: about 2^-23
+// absolute, no quadrant logic.
+constexpr int kSinCosTabN = 1024;
+__shared__ float2 g_sincos_tab[kSinCosTabN];
+
+template <int X>
+__device__ __forceinline__ void xform_prologue() {
+#if PRNG_SINCOS_TAB
+    if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
+        for (int i = threadIdx.x; i < kSinCosTabN; i += blockDim.x) {
+            float sn, cs;
+            sincospif((float)i * (1.0f / 512.0f), &sn, &cs);  // angle 2 pi i / 1024, exact argument
+            g_sincos_tab[i] = make_float2(sn, cs);
+        }
+        __syncthreads();
+    }
+#endif
+}
+
+__device__ __forceinline__ void sincos_2pi_k24_tab(uint32_t k, float& sn, float& cs) {
+    const float2 t = g_sincos_tab[k >> 14];
+    const float x = __uint2float_rn(k & 0x3FFFu) * 3.7450702e-07f;  // 2 pi 2^-24
+    const float x2 = x * x;
+    const float sl = fmaf(x * x2, -0.16666667f, x);
+    const float cl = fmaf(x2, -0.5f, 1.0f);
+    sn = fmaf(t.x, cl, t.y * sl);
+    cs = fmaf(t.y, cl, -(t.x * sl));
+}
+
 // (r, sin, cos) of the fast route; r = sqrt(-2 ln u1') by MUFU.SQRT
 // (relative error <= 2^-23.2, exhaustive).
 __device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, float& r, float& sn, float& cs) {
@@ -531,7 +567,11 @@ __device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, f
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(s2));
     r = s2 > 0.0f ? s2 * rs : 0.0f;
 #endif
+#if PRNG_SINCOS_TAB
+    sincos_2pi_k24_tab(w1 >> 8, sn, cs);
+#else
     sincos_2pi_k24(w1 >> 8, sn, cs);
+#endif
 }
 
 __device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {

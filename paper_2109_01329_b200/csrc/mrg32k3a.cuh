@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
         sj1[i] = a.j1[i / 9][i % 9];
         sj2[i] = a.j2[i / 9][i % 9];
     }
+    xform_prologue<X>();
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;

@@ -196,6 +196,7 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
 
 template <int X, int SHIFT>
 __global__ void __launch_bounds__(kPhiloxThreads) philox_kernel(const PhiloxBody a) {
+    xform_prologue<X>();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gstride = gridDim.x * blockDim.x;
     if (a.s.n) {
