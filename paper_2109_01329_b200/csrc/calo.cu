@@ -79,98 +79,108 @@ __global__ void __launch_bounds__(kCaloThreads)
 
 // numpy's pairwise sum evaluated by a warp: the recursion's leaves (runs of
 // <= 128 elements, each summed exactly as np_pairwise_sum's leaf branch) are
-// independent, so lane l sums leaves l, l + 32, ...; lane 0 then adds the leaf
-// sums back up the same binary tree.  Bit-identical to np_pairwise_sum.
+// independent, so lane 0 lists them once per particle (iterative DFS),
+// lane l sums leaves l, l + 32, ..., and lane 0 adds the leaf sums back up the
+// same binary tree (iterative post-order walk).  Bit-identical to
+// np_pairwise_sum.  All stacks live in shared memory: no local memory, so
+// the kernel carries no per-thread stack reservation.
 constexpr int kNormWarps = 4;
-constexpr int kNormMaxLeaves = 512;  // n <= ~28k per particle; larger: serial
-
-struct LeafRange {
-    uint64_t off, n;
-};
+constexpr int kNormMaxLeaves = 512;  // n <= ~28k per particle in the list; larger: leaves summed by lane 0
+constexpr int kNormStack = 48;      // tree depth <= log2(n / 64) + 1 < 48 for any 64-bit n
 
 __device__ __forceinline__ uint64_t pw_split(uint64_t n) {  // numpy: n2 = n / 2; n2 -= n2 % 8
     const uint64_t n2 = n / 2;
     return n2 - n2 % 8;
 }
 
-// Visit the leaves of np_pairwise_sum(a, n) in order: f(k, off, len); returns
-// the leaf count.  Iterative (explicit stack, depth <= log2(n / 64) + 1).
-template <typename F>
-__device__ __forceinline__ uint32_t for_each_leaf(uint64_t n, F f) {
-    LeafRange st[40];
+struct NormWarpSmem {
+    uint64_t leaf_off[kNormMaxLeaves];
+    uint32_t leaf_len[kNormMaxLeaves];
+    double leaf_val[kNormMaxLeaves];
+    uint64_t st_off[kNormStack], st_n[kNormStack];
+    double st_left[kNormStack];
+    uint32_t st_stage[kNormStack];
+};
+
+// Lane 0: the leaves of np_pairwise_sum(., n) in order; returns their count
+// (entries past kNormMaxLeaves are counted, not stored).
+__device__ uint32_t list_leaves(NormWarpSmem& m, uint64_t n) {
     int sp = 0;
     uint32_t k = 0;
-    st[sp++] = LeafRange{0, n};
+    m.st_off[0] = 0;
+    m.st_n[0] = n;
+    sp = 1;
     while (sp) {
-        const LeafRange r = st[--sp];
-        if (r.n <= 128) {
-            f(k++, r.off, r.n);
+        --sp;
+        const uint64_t off = m.st_off[sp], len = m.st_n[sp];
+        if (len <= 128) {
+            if (k < (uint32_t)kNormMaxLeaves) {
+                m.leaf_off[k] = off;
+                m.leaf_len[k] = (uint32_t)len;
+            }
+            ++k;
             continue;
         }
-        const uint64_t n2 = pw_split(r.n);
-        st[sp++] = LeafRange{r.off + n2, r.n - n2};
-        st[sp++] = LeafRange{r.off, n2};
+        const uint64_t n2 = pw_split(len);
+        m.st_off[sp] = off + n2;
+        m.st_n[sp] = len - n2;
+        ++sp;
+        m.st_off[sp] = off;
+        m.st_n[sp] = n2;
+        ++sp;
     }
     return k;
 }
 
-// Sum the leaf values back up np_pairwise_sum's tree: res = left + right at
-// every internal node (iterative post-order walk); leaf(off, len) supplies
-// the value of each leaf, in order.
-template <typename L>
-__device__ double combine_leaves(uint64_t n, L leaf) {
-    struct Frame {
-        uint64_t off, n;
-        double left;
-        int stage;  // 0 = new, 1 = left child pending, 2 = right child pending
-    };
-    Frame st[40];
+// Lane 0: res = left + right at every internal node of np_pairwise_sum's
+// tree over n elements; leaves take leaf_val[] in order (listed) or are
+// summed on the fly from a (too many leaves for the list).
+__device__ double combine_leaves(NormWarpSmem& m, uint64_t n, const double* a, bool listed) {
     int sp = 0;
-    st[sp++] = Frame{0, n, 0.0, 0};
+    uint32_t kk = 0;
+    m.st_off[0] = 0;
+    m.st_n[0] = n;
+    m.st_stage[0] = 0;
+    sp = 1;
     for (;;) {
-        Frame& t = st[sp - 1];
-        if (t.n > 128) {
-            t.stage = 1;
-            st[sp++] = Frame{t.off, pw_split(t.n), 0.0, 0};
+        const int t = sp - 1;
+        if (m.st_n[t] > 128) {
+            m.st_stage[t] = 1;
+            m.st_off[sp] = m.st_off[t];
+            m.st_n[sp] = pw_split(m.st_n[t]);
+            m.st_stage[sp] = 0;
+            ++sp;
             continue;
         }
-        double val = leaf(t.off, t.n);
+        double val = listed ? m.leaf_val[kk++] : np_leaf_sum(a + m.st_off[t], m.st_n[t]);
         --sp;
         for (;;) {  // deliver val to the parents
             if (sp == 0) return val;
-            Frame& p = st[sp - 1];
-            if (p.stage == 1) {
-                p.left = val;
-                p.stage = 2;
-                const uint64_t n2 = pw_split(p.n);
-                st[sp++] = Frame{p.off + n2, p.n - n2, 0.0, 0};
+            const int q = sp - 1;
+            if (m.st_stage[q] == 1) {
+                m.st_left[q] = val;
+                m.st_stage[q] = 2;
+                const uint64_t n2 = pw_split(m.st_n[q]);
+                m.st_off[sp] = m.st_off[q] + n2;
+                m.st_n[sp] = m.st_n[q] - n2;
+                m.st_stage[sp] = 0;
+                ++sp;
                 break;
             }
-            val = __dadd_rn(p.left, val);
+            val = __dadd_rn(m.st_left[q], val);
             --sp;
         }
     }
 }
 
-// np_pairwise_sum(a, n) on one thread.
-__device__ double np_pairwise_sum(const double* a, uint64_t n) {
-    return combine_leaves(n, [&](uint64_t off, uint64_t len) { return np_leaf_sum(a + off, len); });
-}
-
-__device__ __forceinline__ uint32_t leaf_count(uint64_t n) {
-    return for_each_leaf(n, [](uint32_t, uint64_t, uint64_t) {});
-}
-
-__device__ double warp_pairwise_sum(const double* a, uint64_t n, double* leaf, uint32_t lane) {
-    for_each_leaf(n, [&](uint32_t k, uint64_t off, uint64_t len) {
-        if ((k & 31u) == lane) leaf[k] = np_leaf_sum(a + off, len);
-    });
-    __syncwarp();
-    double r = 0.0;
-    if (lane == 0) {
-        uint32_t k = 0;
-        r = combine_leaves(n, [&](uint64_t, uint64_t) { return leaf[k++]; });
+__device__ double warp_pairwise_sum(NormWarpSmem& m, const double* a, uint64_t n, uint32_t nleaves, uint32_t lane) {
+    const bool listed = nleaves <= (uint32_t)kNormMaxLeaves;
+    if (listed) {
+        for (uint32_t i = lane; i < nleaves; i += 32) m.leaf_val[i] = np_leaf_sum(a + m.leaf_off[i], m.leaf_len[i]);
+        __syncwarp();
     }
+    double r = 0.0;
+    if (lane == 0) r = combine_leaves(m, n, a, listed);
     __syncwarp();
     return __shfl_sync(0xffffffffu, r, 0);
 }
@@ -179,24 +189,21 @@ __device__ double warp_pairwise_sum(const double* a, uint64_t n, double* leaf, u
 __global__ void __launch_bounds__(32 * kNormWarps)
     calo_normalize_kernel(const prng_calo_particle_t* __restrict__ parts, uint32_t nparts,
                           double* __restrict__ hit_amount, double* __restrict__ particle_sums) {
-    __shared__ double leaves[kNormWarps][kNormMaxLeaves];
+    __shared__ NormWarpSmem smem[kNormWarps];
     const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const uint32_t p = blockIdx.x * kNormWarps + w;
     if (p >= nparts) return;  // warp-uniform
+    NormWarpSmem& m = smem[w];
     const prng_calo_particle_t pt = parts[p];
     if (pt.hits == 0) {
         if (lane == 0) particle_sums[p] = 0.0;
         return;
     }
     double* a = hit_amount + pt.hit_offset;
-    const bool par = leaf_count(pt.hits) <= (uint32_t)kNormMaxLeaves;
-    double raw_sum;
-    if (par) {
-        raw_sum = warp_pairwise_sum(a, pt.hits, leaves[w], lane);
-    } else {
-        raw_sum = lane == 0 ? np_pairwise_sum(a, pt.hits) : 0.0;
-        raw_sum = __shfl_sync(0xffffffffu, raw_sum, 0);
-    }
+    uint32_t nleaves = lane == 0 ? list_leaves(m, pt.hits) : 0;
+    nleaves = __shfl_sync(0xffffffffu, nleaves, 0);
+    __syncwarp();
+    const double raw_sum = warp_pairwise_sum(m, a, pt.hits, nleaves, lane);
     if (raw_sum > 0.0) {
         const double scale = pt.target / raw_sum;
         for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = __dmul_rn(a[j], scale);
@@ -205,12 +212,7 @@ __global__ void __launch_bounds__(32 * kNormWarps)
         for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = each;
     }
     __syncwarp();
-    double sum;
-    if (par) {
-        sum = warp_pairwise_sum(a, pt.hits, leaves[w], lane);
-    } else {
-        sum = lane == 0 ? np_pairwise_sum(a, pt.hits) : 0.0;
-    }
+    const double sum = warp_pairwise_sum(m, a, pt.hits, nleaves, lane);
     if (lane == 0) particle_sums[p] = sum;
 }
 
