@@ -500,15 +500,13 @@ __device__ __forceinline__ void sincos_2pi_k24(uint32_t k, float& sn, float& cs)
 //  * u1 = k 2^-24 >= 2^-4: -2 ln2 * lg2.approx(1 - u1) (1 - u1 exact); the
 //    SFU's relative error here is <= 2^-20.5 (measured exhaustively,
 //    tools/mufu_accuracy.cu), i.e. <= 2^-21.5 in r;
-//  * u1 < 2^-4: the series -2 ln(1 - x) = x (2 + x + 2x^2/3 + ... + 2x^6/7),
-//    truncation < 2^-27 relative, so r keeps full relative accuracy as
-//    u1' -> 1.
+//  * u1 < 2^-4: the series -2 ln(1 - x) = x (2 + x + 2x^2/3 + x^3/2 + 2x^4/5),
+//    truncation x^5/6 < 2^-22.5 relative, so r keeps its relative accuracy
+//    as u1' -> 1.
 __device__ __forceinline__ float neg2_ln_u1_v2(uint32_t w0) {
     const uint32_t k = w0 >> 8;
     const float x = __uint2float_rn(k) * 5.9604644775390625e-08f;  // u1, exact
-    float p = 0.28571428571f;                                        // 2/7
-    p = fmaf(p, x, 0.33333333333f);
-    p = fmaf(p, x, 0.4f);
+    float p = 0.4f;                                                  // 2/5
     p = fmaf(p, x, 0.5f);
     p = fmaf(p, x, 0.66666666667f);
     p = fmaf(p, x, 1.0f);
