@@ -676,8 +676,8 @@ template <> __device__ __forceinline__ void xform2<kLognF32Fast>(uint32_t w0, ui
     float r, sn, cs;
     box_muller_f32_parts(w0, w1, r, sn, cs);
     const float rs = r * p.scale_f;
-    o0 = fmaf(expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);
-    o1 = fmaf(expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+    o0 = fmaf(__expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);  // ex2.approx: 2^-21 rel
+    o1 = fmaf(__expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
 }
 
 // Four consecutive stream words -> four outputs.  For pair transforms the

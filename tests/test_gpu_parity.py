@@ -548,3 +548,18 @@ def test_concurrent_host_threads_and_streams():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("m,s,displ,scale", [(0.0, 1.0, 0.0, 1.0), (0.3, 0.7, -1.5, 2.5), (-2.0, 2.5, 0.0, 1.0)])
+def test_lognormal_fast_dense_stream(m, s, displ, scale):
+    """Fast fp32 lognormal (SFU log/sqrt/exp, table sincos) on 2^26 samples
+    (2^25 word pairs, dense over the 24-bit input grids): within the stated
+    tolerance of the oracle (fp64 Box-Muller, libm exp)."""
+    st = P.seed_engine(PHILOX, 4242)
+    n = 1 << 26
+    _, got = P.generate(P.Lognormal(m, s, displ, scale, "fp32", "fast"), st, n)
+    want = O.generate("philox", (O.seed_philox(4242), 0), "lognormal", n, "fp32", m, s, displ=displ, scale=scale)
+    allowed = lognormal_allowed((want.astype(np.float64) - displ) / scale, m, s, np.float32, True) * scale + \
+        4 * np.spacing(np.abs(want)).astype(np.float64)
+    err, exact = check_close(host(got), want, allowed, f"logn fast {m},{s}")
+    print(f"lognormal fast ({m}, {s}, {displ}, {scale}): max abs err {err:.3e}, bit-exact {exact:.4f}")
