@@ -439,62 +439,8 @@ __device__ __forceinline__ double corrected(double approx, int d, const ExactCor
 }
 
 // Fast (fp32) route, specialised to the 24-bit inputs (DESIGN.md
-// "Tolerances"; coefficients fitted and verified exhaustively over all 2^24
-// inputs by tools/fit_boxmuller.py):
-//  * s = -2 ln u1' with u1' = m * 2^-24, m = 2^24 - (w0 >> 8) in [1, 2^24]:
-//    m -> float is exact; split m = f * 2^e with f in [sqrt(1/2), sqrt(2)),
-//    ln f = g + g^2 Q(g) (g = f - 1 exact, Q degree 7), so the relative error
-//    stays ~2 ulp even as u1' -> 1; max rel err 1.96 * 2^-24;
-//  * r = sqrt(s) as s * rsqrt(s) (MUFU.RSQ);
-//  * (cos, sin)(2 pi k / 2^24), k = w1 >> 8: the quadrant comes straight from
-//    the integer (exact argument reduction), the remainder t in [-1, 1) is
-//    exact and cos/sin(pi t / 4) are degree-8/9 polynomials; abs err
-//    1.43 * 2^-24.
-__device__ __forceinline__ float neg2_ln_u1(uint32_t w0) {
-    const float x = (float)(16777216u - (w0 >> 8));  // exact
-    const int ib = __float_as_int(x);
-    const int e = (ib - 0x3F3504F3) >> 23;
-    const float f = __int_as_float(ib - (e << 23));
-    const float g = f - 1.0f;
-    float q = 9.004202485e-02f;
-    q = fmaf(q, g, -1.425779462e-01f);
-    q = fmaf(q, g, 1.480645984e-01f);
-    q = fmaf(q, g, -1.657504737e-01f);
-    q = fmaf(q, g, 1.997310519e-01f);
-    q = fmaf(q, g, -2.500160933e-01f);
-    q = fmaf(q, g, 3.333365917e-01f);
-    q = fmaf(q, g, -4.999999404e-01f);
-    const float lnf = fmaf(g * g, q, g);
-    const float lnx = fmaf((float)(e - 24), 0.6931471805599453f, lnf);
-    return -2.0f * lnx;
-}
-
-__device__ __forceinline__ void sincos_2pi_k24(uint32_t k, float& sn, float& cs) {
-    const uint32_t kk = k + (1u << 21);
-    const uint32_t q = (kk >> 22) & 3u;
-    const float t = (float)((int)(kk & 0x3FFFFFu) - (1 << 21)) * 4.76837158203125e-07f;  // 2^-21, exact
-    const float t2 = t * t;
-    float s = 3.089971017e-07f;
-    s = fmaf(s, t2, -3.657239358e-05f);
-    s = fmaf(s, t2, 2.490393119e-03f);
-    s = fmaf(s, t2, -8.074551076e-02f);
-    s = fmaf(s, t2, 7.853981853e-01f);
-    s *= t;
-    float c = 3.529804189e-06f;
-    c = fmaf(c, t2, -3.259385994e-04f);
-    c = fmaf(c, t2, 1.585432515e-02f);
-    c = fmaf(c, t2, -3.084251285e-01f);
-    c = fmaf(c, t2, 1.0f);
-    const bool swap = q & 1u;
-    const float a = swap ? s : c;
-    const float b = swap ? c : s;
-    cs = __int_as_float(__float_as_int(a) ^ ((((q + 1u) >> 1) & 1u) << 31));
-    sn = __int_as_float(__float_as_int(b) ^ ((q >> 1) << 31));
-}
-
-#ifndef PRNG_BM_FAST_V2
-#define PRNG_BM_FAST_V2 1
-#endif
+// "Tolerances"; accuracy measured exhaustively over the 2^24-point grids,
+// tools/mufu_accuracy.cu and the GPU tests).
 // -2 ln u1' with one SFU op for most inputs (fewer issue slots than the
 // polynomial above; the fast gaussian is issue-bound):
 //  * u1 = k 2^-24 >= 2^-4: -2 ln2 * lg2.approx(1 - u1) (1 - u1 exact); the
@@ -516,9 +462,6 @@ __device__ __forceinline__ float neg2_ln_u1_v2(uint32_t w0) {
     return k < (1u << 20) ? x * p : l2 * -1.3862943611198906f;
 }
 
-#ifndef PRNG_SINCOS_TAB
-#define PRNG_SINCOS_TAB 1
-#endif
 // Fast-route (sin, cos)(2 pi k 2^-24) by angle addition: a per-CTA
 // shared-memory table of (sin, cos)(2 pi j / 1024) (8 KB, filled by the
 // kernel prologue with sincospif) for the top 10 bits of k, and
@@ -530,7 +473,6 @@ __shared__ float2 g_sincos_tab[kSinCosTabN];
 
 template <int X>
 __device__ __forceinline__ void xform_prologue() {
-#if PRNG_SINCOS_TAB
     if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
         for (int i = threadIdx.x; i < kSinCosTabN; i += blockDim.x) {
             float sn, cs;
@@ -539,7 +481,6 @@ __device__ __forceinline__ void xform_prologue() {
         }
         __syncthreads();
     }
-#endif
 }
 
 __device__ __forceinline__ void sincos_2pi_k24_tab(uint32_t k, float& sn, float& cs) {
@@ -555,21 +496,9 @@ __device__ __forceinline__ void sincos_2pi_k24_tab(uint32_t k, float& sn, float&
 // (r, sin, cos) of the fast route; r = sqrt(-2 ln u1') by MUFU.SQRT
 // (relative error <= 2^-23.2, exhaustive).
 __device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, float& r, float& sn, float& cs) {
-#if PRNG_BM_FAST_V2
     const float s2 = neg2_ln_u1_v2(w0);
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s2));  // s2 = 0 or >= 1.19e-7
-#else
-    const float s2 = neg2_ln_u1(w0);
-    // s2 is 0 (u1' = 1) or >= 1.19e-7 (normal): the raw MUFU.RSQ (ftz) is safe.
-    float rs;
-    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rs) : "f"(s2));
-    r = s2 > 0.0f ? s2 * rs : 0.0f;
-#endif
-#if PRNG_SINCOS_TAB
     sincos_2pi_k24_tab(w1 >> 8, sn, cs);
-#else
-    sincos_2pi_k24(w1 >> 8, sn, cs);
-#endif
 }
 
 __device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {

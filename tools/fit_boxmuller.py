@@ -1,6 +1,11 @@
 #!/usr/bin/env python3
 """Fit and exhaustively verify the fp32 polynomials of the fast Box-Muller path.
 
+HISTORICAL: these were the polynomials of the first fast fp32 route; the
+current route uses the SFU log/sqrt and a shared-memory sincos table
+(csrc/common.cuh).  Kept as the record of the
+exhaustive polynomial fits.
+
 Emulates the device arithmetic in numpy float32 (FFMA as float64 fma then
 one rounding to float32) over ALL 2^24 possible 24-bit inputs and reports the
 error against float64 libm.  Prints C constants for common.cuh.
