@@ -1,0 +1,19 @@
+import sys, time
+sys.path.insert(0, '.')
+import numpy as np, torch
+import paper_2109_01329_b200 as P
+from paper_2109_01329_b200 import calosim as C
+nev, regions, ncells = 10000, 24, 190_000
+geom = [np.arange(r, ncells, regions, dtype=np.int64) for r in range(regions)]
+edges = np.linspace(0.001, 0.101, 9)
+weights = np.asarray([0.05, 0.10, 0.20, 0.25, 0.20, 0.10, 0.07, 0.03])
+det = C.Detector(geom, {"electron": C.Parameterization("electron", 4000, 6500, edges, weights)})
+events = C.synth_single_electron_events(nev, 777)
+st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+C.simulate_events(events[:50], det, st, dicts=False)
+for ce in (2048, 1024, 10000, 2048):
+    for i in range(8):
+        t0 = time.perf_counter()
+        final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=ce)
+        torch.cuda.synchronize()
+        print(ce, f"{(time.perf_counter()-t0)*1e3:.1f} ms")
