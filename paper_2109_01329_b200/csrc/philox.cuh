@@ -195,17 +195,18 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
 }
 
 // Minimum resident CTAs per SM given to ptxas.  For the unit / [a, b) fp32
-// kernels (C1/C4) a bound of 5 lets ptxas use 48 registers and schedule the
-// four blocks' multiply chains further apart: occupancy 5 instead of 6 but
-// +3.5-4% throughput (measured); the other transforms keep
-// ptxas' default (0 = no bound).
-template <int X>
+// kernels (C1/C4) a bound of 5 (4 for the funnel variants) lets ptxas use
+// ~48 registers and schedule the four blocks' multiply chains further
+// apart: occupancy 5 instead of 6 but +3.5-4% throughput (+6% for the
+// funnel), measured; the other transforms keep ptxas'
+// default (0 = no bound).  Eight blocks per thread measured 20% slower.
+template <int X, int SHIFT>
 constexpr int philox_min_blocks() {
-    return (X == kUnitF32 || X == kUniformF32) ? 5 : 0;
+    return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? 5 : 4) : 0;
 }
 
 template <int X, int SHIFT>
-__global__ void __launch_bounds__(kPhiloxThreads, philox_min_blocks<X>()) philox_kernel(const PhiloxBody a) {
+__global__ void __launch_bounds__(kPhiloxThreads, philox_min_blocks<X, SHIFT>()) philox_kernel(const PhiloxBody a) {
     xform_prologue<X>();
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gstride = gridDim.x * blockDim.x;
