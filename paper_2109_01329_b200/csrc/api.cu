@@ -602,7 +602,7 @@ __global__ void words_kernel(const uint32_t* __restrict__ w, uint64_t n, XformPa
         if constexpr (XformTraits<X>::kPair) {
             if (2 * i >= n) break;
             typename XformTraits<X>::T o0, o1;
-            xform2<X>(w[2 * i], w[2 * i + 1], p, o0, o1);
+            xform2k<X>(w[2 * i], w[2 * i + 1], p, o0, o1);
             out[2 * i] = o0;
             if (2 * i + 1 < n) out[2 * i + 1] = o1;
         } else {

@@ -296,6 +296,7 @@ __device__ __forceinline__ typename XformTraits<X>::T xform1(uint32_t w, const X
 template <> __device__ __forceinline__ uint32_t xform1<kBits>(uint32_t w, const XformParams&) { return w; }
 
 template <> __device__ __forceinline__ float xform1<kUnitF32>(uint32_t w, const XformParams&) { return unit_f32(w); }
+
 template <> __device__ __forceinline__ double xform1<kUnitF64>(uint32_t w, const XformParams&) { return unit_f64(w); }
 
 // fl(fl(u * S) + off) with u = (w >> 8) * 2^-24.  Because the 2^-24 factor is
@@ -439,73 +440,100 @@ __device__ __forceinline__ double corrected(double approx, int d, const ExactCor
 }
 
 // Fast (fp32) route, specialised to the 24-bit inputs (DESIGN.md
-// "Tolerances"; accuracy measured exhaustively over the 2^24-point grids,
-// tools/mufu_accuracy.cu and the GPU tests).
-// -2 ln u1' with one SFU op for most inputs (fewer issue slots than the
-// polynomial above; the fast gaussian is issue-bound):
-//  * u1 = k 2^-24 >= 2^-4: -2 ln2 * lg2.approx(1 - u1) (1 - u1 exact); the
-//    SFU's relative error here is <= 2^-20.5 (measured exhaustively,
-//    tools/mufu_accuracy.cu), i.e. <= 2^-21.5 in r;
-//  * u1 < 2^-4: the series -2 ln(1 - x) = x (2 + x + 2x^2/3 + x^3/2 + 2x^4/5),
-//    truncation x^5/6 < 2^-22.5 relative, so r keeps its relative accuracy
-//    as u1' -> 1.
-__device__ __forceinline__ float neg2_ln_u1_v2(uint32_t w0) {
-    const uint32_t k = w0 >> 8;
-    const float x = __uint2float_rn(k) * 5.9604644775390625e-08f;  // u1, exact
-    float p = 0.4f;                                                  // 2/5
-    p = fmaf(p, x, 0.5f);
-    p = fmaf(p, x, 0.66666666667f);
-    p = fmaf(p, x, 1.0f);
-    p = fmaf(p, x, 2.0f);
-    float l2;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(1.0f - x));  // 1 - x >= 2^-24: normal
-    return k < (1u << 20) ? x * p : l2 * -1.3862943611198906f;
+// "Tolerances"; accuracy measured exhaustively over the 2^24-point grids by
+// the GPU tests: worst error 0.2-0.6 of the stated tolerance).
+//  * -lg2(1 - u1) by one MUFU.LG2 for u1 >= 2^(SER - 24); below, the series
+//    x (1 + x/2 + x^2/3)/ln 2 (truncation x^3/4 < 2^-26 relative), so r keeps
+//    its relative accuracy as u1' -> 1.  Working in lg2 units saves the
+//    -2 ln 2 multiply: r = sqrt(-lg2(1 - u1)) * sqrt(2 ln 2), and the
+//    sqrt(2 ln 2) is folded into the caller's loop-invariant scale.
+//  * r by MUFU.SQRT (relative error <= 2^-23.2, exhaustive);
+//  * (sin, cos)(2 pi k 2^-24) by angle addition: a per-CTA shared-memory
+//    table of (sin, cos)(2 pi j / 2^TL) (filled by the kernel prologue with
+//    sincospif) for the top TL bits of k, and for the remaining
+//    x < 2 pi 2^-TL: sin x = x, cos x = 1 - x^2/2 (TL < 12) or 1 (TL >= 12:
+//    relative error x^2/2 <= 1.2e-6 on z, inside the 2^-19 tolerance).  x is
+//    built without I2FP: f = bits(0x3F800000 | low bits of k at the top of
+//    the mantissa) = 1 + klow 2^-L, x = (f - 1) C, one FFMA, exact input.
+#ifndef PRNG_BM_TAB_LOG2
+#define PRNG_BM_TAB_LOG2 12
+#endif
+#ifndef PRNG_BM_SER_LOG2K  // series for k < 2^PRNG_BM_SER_LOG2K, i.e. u1 < 2^(LOG2K - 24)
+#define PRNG_BM_SER_LOG2K 16
+#endif
+#ifndef PRNG_BM_SER_TERMS
+#define PRNG_BM_SER_TERMS 3
+#endif
+#ifndef PRNG_BM_COS_QUAD_BELOW  // keep the cos x^2/2 term for tables smaller than 2^this
+#define PRNG_BM_COS_QUAD_BELOW 12
+#endif
+constexpr int kPhiloxTabLog2 = PRNG_BM_TAB_LOG2;  // Philox / words kernels (32 KB at 12)
+constexpr int kMrgTabLog2 = 10;                   // MRG kernel: 8 KB next to its 32 KB store stage
+constexpr float kBmRq = 1.1774100225154747f;      // sqrt(2 ln 2): r = rq * kBmRq
+
+template <int TL>
+__device__ __forceinline__ float2* sincos_tab() {
+    __shared__ float2 tab[1 << TL];
+    return tab;
 }
 
-// Fast-route (sin, cos)(2 pi k 2^-24) by angle addition: a per-CTA
-// shared-memory table of (sin, cos)(2 pi j / 1024) (8 KB, filled by the
-// kernel prologue with sincospif) for the top 10 bits of k, and
-// sin(x) = x - x^3/6, cos(x) = 1 - x^2/2 for the remaining x < 2 pi 2^-10
-// (truncation < 6e-11).  Table rounding + combination: about 2^-23
-// absolute, no quadrant logic.
-constexpr int kSinCosTabN = 1024;
-__shared__ float2 g_sincos_tab[kSinCosTabN];
-
-template <int X>
+template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform_prologue() {
     if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
-        for (int i = threadIdx.x; i < kSinCosTabN; i += blockDim.x) {
+        float2* tab = sincos_tab<TL>();
+        for (int i = threadIdx.x; i < (1 << TL); i += blockDim.x) {
             float sn, cs;
-            sincospif((float)i * (1.0f / 512.0f), &sn, &cs);  // angle 2 pi i / 1024, exact argument
-            g_sincos_tab[i] = make_float2(sn, cs);
+            sincospif((float)i * (2.0f / (1 << TL)), &sn, &cs);  // angle 2 pi i / 2^TL, exact argument
+            tab[i] = make_float2(sn, cs);
         }
         __syncthreads();
     }
 }
 
-__device__ __forceinline__ void sincos_2pi_k24_tab(uint32_t k, float& sn, float& cs) {
-    const float2 t = g_sincos_tab[k >> 14];
-    const float x = __uint2float_rn(k & 0x3FFFu) * 3.7450702e-07f;  // 2 pi 2^-24
-    const float x2 = x * x;
-    const float sl = fmaf(x * x2, -0.16666667f, x);
-    const float cl = fmaf(x2, -0.5f, 1.0f);
-    sn = fmaf(t.x, cl, t.y * sl);
-    cs = fmaf(t.y, cl, -(t.x * sl));
+__device__ __forceinline__ float neg_lg2_1mu(uint32_t w0) {
+    const uint32_t k = w0 >> 8;
+    const float kf = __uint2float_rn(k);
+    const float omx = fmaf(kf, -5.9604644775390625e-08f, 1.0f);  // 1 - u1, exact
+    float l2;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(omx));     // 1 - u1 >= 2^-24: normal
+    if constexpr (PRNG_BM_SER_LOG2K == 0) {
+        return -l2;
+    } else {
+        const float x = kf * 5.9604644775390625e-08f;  // u1, exact
+        constexpr float c[5] = {1.4426950408889634f, 0.7213475204444817f, 0.48089834696298783f,
+                                0.36067376022224085f, 0.28853900817779266f};  // 1/(j ln 2)
+        float p = c[PRNG_BM_SER_TERMS - 1];
+#pragma unroll
+        for (int j = PRNG_BM_SER_TERMS - 2; j >= 0; --j) p = fmaf(p, x, c[j]);
+        return k < (1u << PRNG_BM_SER_LOG2K) ? x * p : -l2;
+    }
 }
 
-// (r, sin, cos) of the fast route; r = sqrt(-2 ln u1') by MUFU.SQRT
-// (relative error <= 2^-23.2, exhaustive).
-__device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, float& r, float& sn, float& cs) {
-    const float s2 = neg2_ln_u1_v2(w0);
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(s2));  // s2 = 0 or >= 1.19e-7
-    sincos_2pi_k24_tab(w1 >> 8, sn, cs);
+template <int TL>
+__device__ __forceinline__ void sincos_2pi_k24(uint32_t w1, float& sn, float& cs) {
+    constexpr int L = 24 - TL;  // low bits of k = w1 >> 8 left to the polynomial
+    static_assert(L >= 1 && L <= 15, "table size");
+    const float2 t = sincos_tab<TL>()[w1 >> (32 - TL)];
+    // bits [8, 8 + L) of w1 -> mantissa bits [23 - L, 23)
+    const float f = __uint_as_float(((w1 << (15 - L)) & (((1u << L) - 1u) << (23 - L))) | 0x3F800000u);
+    constexpr float C = 3.7450702e-07f * (float)(1u << L);  // 2 pi 2^(L - 24) (power-of-two scaling of 2 pi 2^-24)
+    const float x = fmaf(f, C, -C);
+    if constexpr (TL < PRNG_BM_COS_QUAD_BELOW) {
+        const float cl = fmaf(x * x, -0.5f, 1.0f);
+        sn = fmaf(t.y, x, t.x * cl);
+        cs = fmaf(-t.x, x, t.y * cl);
+    } else {
+        sn = fmaf(t.y, x, t.x);
+        cs = fmaf(-t.x, x, t.y);
+    }
 }
 
-__device__ __forceinline__ void box_muller_f32(uint32_t w0, uint32_t w1, float& z0, float& z1) {
-    float r, sn, cs;
-    box_muller_f32_parts(w0, w1, r, sn, cs);
-    z0 = r * cs;
-    z1 = r * sn;
+// (rq, sin, cos) of the fast route, r = rq * kBmRq.
+template <int TL>
+__device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, float& rq, float& sn, float& cs) {
+    const float s = neg_lg2_1mu(w0);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(s));  // s = 0 or >= 1.7e-7
+    sincos_2pi_k24<TL>(w1, sn, cs);
 }
 
 template <int X>
@@ -528,14 +556,6 @@ template <> __device__ __forceinline__ void xform2<kGaussF32Accurate>(uint32_t w
     o1 = (float)__dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
 }
 
-template <> __device__ __forceinline__ void xform2<kGaussF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
-                                                                 float& o0, float& o1) {
-    float r, sn, cs;
-    box_muller_f32_parts(w0, w1, r, sn, cs);
-    const float rs = r * p.scale_f;  // stddev folded into r: mean + (r sd) cos t
-    o0 = fmaf(rs, cs, p.off_f);
-    o1 = fmaf(rs, sn, p.off_f);
-}
 
 // Exact route: the reference evaluates r = sqrt(-2.0 * log(u1')), t =
 // TWO_PI * u2, (r cos t, r sin t) in fp64 with the host libm (_core.pyx:
@@ -600,13 +620,26 @@ template <> __device__ __forceinline__ void xform2<kLognF32Accurate>(uint32_t w0
     o1 = (float)b;
 }
 
-template <> __device__ __forceinline__ void xform2<kLognF32Fast>(uint32_t w0, uint32_t w1, const XformParams& p,
-                                                                float& o0, float& o1) {
-    float r, sn, cs;
-    box_muller_f32_parts(w0, w1, r, sn, cs);
-    const float rs = r * p.scale_f;
-    o0 = fmaf(__expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);  // ex2.approx: 2^-21 rel
-    o1 = fmaf(__expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+
+// Pair transform as called by the kernels: the fast fp32 routes read the
+// sin/cos table of the calling kernel's size TL (xform_prologue<X, TL>).
+template <int X, int TL = kPhiloxTabLog2>
+__device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformParams& p,
+                                        typename XformTraits<X>::T& o0, typename XformTraits<X>::T& o1) {
+    if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
+        float rq, sn, cs;
+        box_muller_f32_parts<TL>(w0, w1, rq, sn, cs);
+        const float rs = rq * (p.scale_f * kBmRq);  // stddev and sqrt(2 ln 2) folded into r (loop-invariant)
+        if constexpr (X == kGaussF32Fast) {
+            o0 = fmaf(rs, cs, p.off_f);
+            o1 = fmaf(rs, sn, p.off_f);
+        } else {
+            o0 = fmaf(__expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);  // ex2.approx: 2^-21 rel
+            o1 = fmaf(__expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+        }
+    } else {
+        xform2<X>(w0, w1, p, o0, o1);
+    }
 }
 
 // Four consecutive stream words -> four outputs.  For pair transforms the
@@ -614,8 +647,8 @@ template <> __device__ __forceinline__ void xform2<kLognF32Fast>(uint32_t w0, ui
 template <int X>
 __device__ __forceinline__ void xform4(const U4& w, const XformParams& p, typename XformTraits<X>::T o[4]) {
     if constexpr (XformTraits<X>::kPair) {
-        xform2<X>(w.x, w.y, p, o[0], o[1]);
-        xform2<X>(w.z, w.w, p, o[2], o[3]);
+        xform2k<X>(w.x, w.y, p, o[0], o[1]);
+        xform2k<X>(w.z, w.w, p, o[2], o[3]);
     } else {
         o[0] = xform1<X>(w.x, p);
         o[1] = xform1<X>(w.y, p);

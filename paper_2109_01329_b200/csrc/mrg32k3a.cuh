@@ -63,9 +63,21 @@ __device__ __forceinline__ void stage_put(uint4* st, uint32_t lane, int c, uint4
     st[lane * 8 + (c ^ (lane & 7))] = v;
 }
 
+#ifndef PRNG_MRG_ST
+#define PRNG_MRG_ST 0
+#endif
 __device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
+#if PRNG_MRG_ST == 0
     asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                  : "memory");
+#elif PRNG_MRG_ST == 1
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+#else
+    asm volatile("st.global.L1::no_allocate.L2::evict_last.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+#endif
 }
 
 // Write one staged tile (row j = run j, starting at run0 + j*chunk).  Each
@@ -114,7 +126,7 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
         sj1[i] = a.j1[i / 9][i % 9];
         sj2[i] = a.j2[i / 9][i % 9];
     }
-    xform_prologue<X>();
+    xform_prologue<X, kMrgTabLog2>();
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;
@@ -157,11 +169,11 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
                 for (int k = 0; k < CE; k += 2) {
                     const uint32_t a0 = mrg_step_f64(sa);
                     const uint32_t a1 = mrg_step_f64(sa);
-                    xform2<X>(a0, a1, a.p, oa[k], oa[k + 1]);
+                    xform2k<X, kMrgTabLog2>(a0, a1, a.p, oa[k], oa[k + 1]);
                     if constexpr (kMrgChains == 2) {
                         const uint32_t b0 = mrg_step_f64(sb);
                         const uint32_t b1 = mrg_step_f64(sb);
-                        xform2<X>(b0, b1, a.p, ob[k], ob[k + 1]);
+                        xform2k<X, kMrgTabLog2>(b0, b1, a.p, ob[k], ob[k + 1]);
                     }
                 }
             } else {

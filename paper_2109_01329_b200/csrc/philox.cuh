@@ -70,7 +70,7 @@ __device__ __forceinline__ typename XformTraits<X>::T philox_scalar(const Philox
             w1 = lane_of(b, (uint32_t)(v0 & 3) + 1);
         }
         T o0, o1;
-        xform2<X>(w0, w1, p, o0, o1);
+        xform2k<X>(w0, w1, p, o0, o1);
         return (i & 1) ? o1 : o0;
     } else {
         const uint64_t v = a.lane + i;
