@@ -13,6 +13,7 @@
 #include <map>
 #include <mutex>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "../../include/prng_b200.h"
@@ -480,28 +481,44 @@ int check_mrg_state(const uint32_t* s1, const uint32_t* s2) {
 
 struct MrgTables {
     uint32_t nbits;
-    uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];
-    uint32_t h1[9], h2[9];  // A^(chunk/2)
+    uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];  // A^(seg * 2^b)
+    uint32_t h1[9], h2[9];                              // A^(32*chunk/kMrgChains)
+    MrgJump b1, b2;                                     // A^(31*seg), split
 };
 std::mutex g_mrg_mu;
-std::map<std::pair<uint64_t, uint32_t>, MrgTables> g_mrg_tables;
+std::map<std::tuple<uint64_t, uint64_t, uint32_t>, MrgTables> g_mrg_tables;
+
+// B = hi*2^16 + lo with B's entries as symmetric residues mod m.
+MrgJump split_jump(const Mat3& b, uint64_t m) {
+    MrgJump j{};
+    for (int e = 0; e < 9; ++e) {
+        const int64_t v = b.v[e] > m / 2 ? (int64_t)b.v[e] - (int64_t)m : (int64_t)b.v[e];
+        const int64_t hi = (v >= 0 ? v + 32768 : v - 32767) / 65536;  // round to nearest
+        j.hi[e] = (double)hi;
+        j.lo[e] = (double)(v - hi * 65536);
+    }
+    return j;
+}
 
 // Returned by value: another thread may evict the cache entry right after
 // the lock is released.
-MrgTables mrg_tables(uint64_t chunk, uint32_t nbits) {
+MrgTables mrg_tables(uint64_t chunk, uint64_t seg, uint32_t nbits) {
     std::lock_guard<std::mutex> lk(g_mrg_mu);
-    auto key = std::make_pair(chunk, nbits);
+    auto key = std::make_tuple(chunk, seg, nbits);
     auto it = g_mrg_tables.find(key);
     if (it != g_mrg_tables.end()) return it->second;
     MrgTables t{};
     t.nbits = nbits;
     Mat3 a, b;
-    mat_pow_u64(chunk / 2, &a, &b);
+    mat_pow_u64(32 * chunk / kMrgChains, &a, &b);
     for (int e = 0; e < 9; ++e) {
         t.h1[e] = (uint32_t)a.v[e];
         t.h2[e] = (uint32_t)b.v[e];
     }
-    mat_pow_u64(chunk, &a, &b);
+    mat_pow_u64(31 * seg, &a, &b);
+    t.b1 = split_jump(a, kMrgM1);
+    t.b2 = split_jump(b, kMrgM2);
+    mat_pow_u64(seg, &a, &b);
     for (uint32_t i = 0; i < nbits; ++i) {
         for (int e = 0; e < 9; ++e) {
             t.j1[i][e] = (uint32_t)a.v[e];
@@ -530,14 +547,20 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     int sms = 0, occ = 0;
     rc = resident_ctas(kern, kMrgThreads, &sms, &occ);
     if (rc) return rc;
+    // A lane's share `chunk` is a whole number of segments per chain, so
+    // every chain region is whole rounds (MrgPlan: segments of 4 tiles, or
+    // one segment of chunk / kMrgChains words).
     const uint64_t tmax = (uint64_t)sms * occ * kMrgThreads;
     uint64_t chunk = (n + tmax - 1) / tmax;
-    chunk = (chunk + kMrgChains * TW - 1) / (kMrgChains * TW) * (kMrgChains * TW);  // chains x whole tiles
+    const uint64_t unit = MrgPlan<X>::kSegmented ? kMrgChains * 4 * TW : kMrgChains * TW;
+    chunk = (chunk + unit - 1) / unit * unit;
+    const uint64_t seg = MrgPlan<X>::kSegmented ? 4 * TW : chunk / kMrgChains;
     const uint64_t tact = (n + chunk - 1) / chunk;
+    const uint64_t qmax = ((tact - 1) / 32) * 32 * chunk / seg + 31;  // last lane's first segment
     uint32_t nbits = 0;
-    while (nbits < 64 && ((tact - 1) >> nbits) != 0) ++nbits;
+    while (nbits < 64 && (qmax >> nbits) != 0) ++nbits;
     if (nbits > (uint32_t)kMrgMaxBits) return fail(PRNG_ERR_INVALID_PARAMETER, "request too large");
-    const MrgTables tb = mrg_tables(chunk, nbits);
+    const MrgTables tb = mrg_tables(chunk, seg, nbits);
     MrgLaunch a{};
     for (int i = 0; i < 3; ++i) {
         a.s1[i] = s1[i];
@@ -545,11 +568,14 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     }
     a.n = n;
     a.chunk = chunk;
+    a.seg = seg;
     a.nbits = nbits;
     memcpy(a.j1, tb.j1, sizeof a.j1);
     memcpy(a.j2, tb.j2, sizeof a.j2);
     memcpy(a.h1, tb.h1, sizeof a.h1);
     memcpy(a.h2, tb.h2, sizeof a.h2);
+    a.b1 = tb.b1;
+    a.b2 = tb.b2;
     a.out = dptr;
     a.p = p;
     const uint64_t blocks = (tact + kMrgThreads - 1) / kMrgThreads;

@@ -1,17 +1,30 @@
-// mrg32k3a.cuh -- MRG32k3a generate+transform kernel with per-thread
+// mrg32k3a.cuh -- MRG32k3a generate+transform kernel with per-lane
 // jump-ahead (sm_100a).
 //
 // Replaces the strictly sequential reference loop _core.pyx:74-102
 // (mrg_fill), which the reference cannot split (rngburn.py:123,
-// engine.py:201-202).  Thread t owns words [t*chunk, (t+1)*chunk) of the
-// request.  Its start state is A^(t*chunk) s0, assembled from the host-built
-// table J_b = A^(chunk * 2^b) mod m (b < nbits), staged in shared memory:
-// one 3x3 mod-m mat-vec per set bit of t.  The chunk is run as two halves
-// (second start = A^(chunk/2) x first start) whose recurrences are
-// interleaved step by step, so every thread carries two independent
-// dependency chains.  Each 128-byte tile of both halves is transposed
-// through an XOR-swizzled shared-memory stage (16-byte chunks) so the warp
-// writes four runs' whole 128-byte lines per 128-bit store instruction.
+// engine.py:201-202).
+//
+// Layout ("segmented rows").  Warp w owns the region [w*32*chunk,
+// (w+1)*32*chunk) of the request, cut into kMrgChains halves, one per
+// interleaved recurrence ("chain") of every lane.  A chain's half is walked
+// in rounds of 32 segments of `seg` words (seg = 4 tiles = 512 bytes of
+// output for the plain fp64 transforms, MrgPlan); in each round lane L produces the segment [round*32*seg + L*seg,
+// +seg) and then jumps its state 31*seg words ahead (x -> B x mod m, B =
+// A^(31 seg) split into 16-bit halves so the 3x3 mat-vec is exact in fp64).
+// So at any time a warp writes one 16 KB contiguous window per chain.  The
+// earlier layout -- one contiguous chunk per lane, 32 write fronts per warp
+// `chunk` words apart -- capped the same stores at 4.5 TB/s on B200 against
+// 6.0 TB/s for windows of 512-byte segments (tools/mrg_pattern.cu,
+// profiles/r1_mrg_pattern.txt).
+//
+// Lane start states are A^(q*seg) s0 with q = (region start)/seg + L,
+// assembled from host tables J_b = A^(seg*2^b) staged in shared memory (one
+// 3x3 mod-m mat-vec per set bit of q); the second chain starts from the
+// first by the host matrix A^(32*chunk/kMrgChains).  Each 128-byte tile of
+// every segment is transposed through an XOR-swizzled shared-memory stage
+// (16-byte chunks) so each 128-bit store instruction writes four segments'
+// whole 128-byte lines.
 #pragma once
 
 #include "common.cuh"
@@ -23,23 +36,62 @@ constexpr int kMrgThreads = 128;
 #ifndef PRNG_MRG_MINB
 #define PRNG_MRG_MINB 6
 #endif
-constexpr int kMrgMinBlocks = PRNG_MRG_MINB;
 #ifndef PRNG_MRG_CHAINS
 #define PRNG_MRG_CHAINS 2
 #endif
 constexpr int kMrgChains = PRNG_MRG_CHAINS;  // interleaved recurrences per thread (1 or 2)
 
+// Segmented rows (seg = 4 tiles, a jump every seg words) pay off where the
+// store pattern is the bound: the plain 8-byte transforms.  Elsewhere (4-byte
+// outputs at <= 3.6 TB/s, the Box-Muller transforms) the jumps cost more than
+// the pattern, and seg = chunk / kMrgChains gives one round per lane (no
+// jumps).  The 8-byte kernels take a 5-CTA bound (no spills with the jump
+// temporaries), the others 6.
+template <int X>
+struct MrgPlan {
+    static constexpr bool kSegmented = sizeof(typename XformTraits<X>::T) == 8 && !XformTraits<X>::kPair;
+    static constexpr int kMinBlocks = kSegmented ? PRNG_MRG_MINB - 1 : PRNG_MRG_MINB;
+};
+
+// Jump matrix B (entries as symmetric residues) split as B = hi*2^16 + lo,
+// |hi|, |lo| <= 2^15: every product with a symmetric state value is below
+// 2^46.1 and every row sum below 2^47.7, exact in fp64.
+struct MrgJump {
+    double hi[9], lo[9];
+};
+
 struct MrgLaunch {
     uint32_t s1[3], s2[3];
     uint64_t n;
-    uint64_t chunk;  // words per thread (multiple of 2 tiles)
+    uint64_t chunk;  // words per lane (region of a warp = 32*chunk; multiple of kMrgChains*seg)
+    uint64_t seg;    // words per lane segment (4 tiles)
     uint32_t nbits;
-    uint32_t j1[kMrgMaxBits][9];
+    uint32_t j1[kMrgMaxBits][9];  // A^(seg * 2^b)
     uint32_t j2[kMrgMaxBits][9];
-    uint32_t h1[9], h2[9];  // A^(chunk/2)
+    uint32_t h1[9], h2[9];  // A^(32*chunk/kMrgChains): chain 0 -> chain 1
+    MrgJump b1, b2;         // A^(31*seg): end of a segment -> start of the lane's next one
     void* out;
     XformParams p;
 };
+
+__device__ __forceinline__ void mrg_jump(const MrgJump& B, double m, double inv_m, double& x0, double& x1,
+                                         double& x2) {
+    double y[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double l = __fma_rn(B.lo[3 * i + 2], x2, __fma_rn(B.lo[3 * i + 1], x1, __dmul_rn(B.lo[3 * i], x0)));
+        const double h = __fma_rn(B.hi[3 * i + 2], x2, __fma_rn(B.hi[3 * i + 1], x1, __dmul_rn(B.hi[3 * i], x0)));
+        y[i] = mrg_reduce(__fma_rn(mrg_reduce(h, m, inv_m), 65536.0, l), m, inv_m);
+    }
+    x0 = y[0];
+    x1 = y[1];
+    x2 = y[2];
+}
+
+__device__ __forceinline__ void mrg_jump_state(const MrgLaunch& a, MrgStateF64& s) {
+    mrg_jump(a.b1, (double)kMrgM1, 1.0 / (double)kMrgM1, s.x10, s.x11, s.x12);
+    mrg_jump(a.b2, (double)kMrgM2, 1.0 / (double)kMrgM2, s.x20, s.x21, s.x22);
+}
 
 template <typename T> struct MrgTile { static constexpr int kWords = 32; };
 template <> struct MrgTile<double> { static constexpr int kWords = 16; };
@@ -80,22 +132,22 @@ __device__ __forceinline__ void st_global_cs_v4(void* p, uint4 v) {
 #endif
 }
 
-// Write one staged tile (row j = run j, starting at run0 + j*chunk).  Each
-// instruction moves four runs' 128-byte lines: lane L handles row
+// Write one staged tile (row j = lane j's segment, starting at run0 + j*rs).
+// Each instruction moves four rows' 128-byte lines: lane L handles row
 // 4i + (L >> 3), chunk L & 7.  The common case (tile entirely inside the
 // request, 16-byte aligned output) is a straight-line block of 8 LDS.128 +
 // 8 STG.128 with one 64-bit stride add each; the predicated element path
 // only runs for the request's last tiles.
 template <typename T>
-__device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ run0, uint64_t chunk, uint32_t lane,
+__device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ run0, uint64_t rs, uint32_t lane,
                                                uint64_t first_elem, uint64_t n, bool vec_ok) {
     constexpr int CE = 16 / sizeof(T);
     constexpr int TW = 8 * CE;
     const uint32_t x = lane & 7;
     const uint32_t r0 = lane >> 3;
-    T* p = run0 + r0 * chunk + x * CE;
-    const uint64_t stride = 4 * chunk;
-    if (vec_ok && first_elem + 31 * chunk + TW <= n) {  // warp-uniform
+    T* p = run0 + r0 * rs + x * CE;
+    const uint64_t stride = 4 * rs;
+    if (vec_ok && first_elem + 31 * rs + TW <= n) {  // warp-uniform
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const uint32_t j = 4 * i + r0;
@@ -103,7 +155,7 @@ __device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ 
         }
         return;
     }
-    uint64_t e = first_elem + r0 * chunk + x * CE;
+    uint64_t e = first_elem + r0 * rs + x * CE;
     for (int i = 0; i < 8; ++i, p += stride, e += stride) {
         const uint32_t j = 4 * i + r0;
         const uint4 v = st[j * 8 + (x ^ (j & 7))];
@@ -115,7 +167,7 @@ __device__ __forceinline__ void mrg_store_tile(const uint4* st, T* __restrict__ 
 }
 
 template <int X>
-__global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const MrgLaunch a) {
+__global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kernel(const MrgLaunch a) {
     using T = typename XformTraits<X>::T;
     constexpr int TW = MrgTile<T>::kWords;
     constexpr int WARPS = kMrgThreads / 32;
@@ -131,13 +183,14 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
 
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = threadIdx.x >> 5;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint64_t t_warp0 = t - lane;
-    if (t_warp0 * a.chunk >= a.n) return;  // whole warp idle (warp-uniform)
+    const uint64_t t_warp0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    const uint64_t w0 = t_warp0 * a.chunk;  // first word of the warp's region
+    if (w0 >= a.n) return;                  // whole warp idle (warp-uniform)
 
+    const uint64_t q = w0 / a.seg + lane;  // lane's first segment, in units of seg
     uint32_t x10 = a.s1[0], x11 = a.s1[1], x12 = a.s1[2], x20 = a.s2[0], x21 = a.s2[1], x22 = a.s2[2];
     for (uint32_t b = 0; b < a.nbits; ++b) {
-        if ((t >> b) & 1) {
+        if ((q >> b) & 1) {
             mat3_apply<kMrgC1>(&sj1[9 * b], x10, x11, x12);
             mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
         }
@@ -152,46 +205,53 @@ __global__ void __launch_bounds__(kMrgThreads, kMrgMinBlocks) mrg_kernel(const M
                          mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
     }
 
-    const uint64_t half = a.chunk / kMrgChains;
+    const uint64_t half = 32 * a.chunk / kMrgChains;  // words per chain region
+    const uint64_t seg = a.seg;
     T* __restrict__ out = static_cast<T*>(a.out);
     uint4* sta = stage[0][warp];
     uint4* stb = stage[kMrgChains - 1][warp];
     const bool vec_ok = ((uintptr_t)out & 15u) == 0;
-    const uint64_t warp_elem0 = t_warp0 * a.chunk;
     constexpr int CE = 16 / sizeof(T);  // elements per 16-byte chunk
-    for (uint64_t off = 0; off < half; off += TW) {
-        if (warp_elem0 + off >= a.n) break;  // warp-uniform
+    for (uint64_t rb = 0; rb < half; rb += 32 * seg) {
+        if (w0 + rb >= a.n) break;  // warp-uniform
+        for (uint64_t off = 0; off < seg; off += TW) {
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            T oa[CE], ob[CE];
-            if constexpr (XformTraits<X>::kPair) {
+            for (int c = 0; c < 8; ++c) {
+                T oa[CE], ob[CE];
+                if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
-                for (int k = 0; k < CE; k += 2) {
-                    const uint32_t a0 = mrg_step_f64(sa);
-                    const uint32_t a1 = mrg_step_f64(sa);
-                    xform2k<X, kMrgTabLog2>(a0, a1, a.p, oa[k], oa[k + 1]);
-                    if constexpr (kMrgChains == 2) {
-                        const uint32_t b0 = mrg_step_f64(sb);
-                        const uint32_t b1 = mrg_step_f64(sb);
-                        xform2k<X, kMrgTabLog2>(b0, b1, a.p, ob[k], ob[k + 1]);
+                    for (int k = 0; k < CE; k += 2) {
+                        const uint32_t a0 = mrg_step_f64(sa);
+                        const uint32_t a1 = mrg_step_f64(sa);
+                        xform2k<X, kMrgTabLog2>(a0, a1, a.p, oa[k], oa[k + 1]);
+                        if constexpr (kMrgChains == 2) {
+                            const uint32_t b0 = mrg_step_f64(sb);
+                            const uint32_t b1 = mrg_step_f64(sb);
+                            xform2k<X, kMrgTabLog2>(b0, b1, a.p, ob[k], ob[k + 1]);
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < CE; ++k) {
+                        oa[k] = xform1<X>(mrg_step_f64(sa), a.p);
+                        if constexpr (kMrgChains == 2) ob[k] = xform1<X>(mrg_step_f64(sb), a.p);
                     }
                 }
-            } else {
-#pragma unroll
-                for (int k = 0; k < CE; ++k) {
-                    oa[k] = xform1<X>(mrg_step_f64(sa), a.p);
-                    if constexpr (kMrgChains == 2) ob[k] = xform1<X>(mrg_step_f64(sb), a.p);
-                }
+                stage_put(sta, lane, c, pack16<T>(oa));
+                if constexpr (kMrgChains == 2) stage_put(stb, lane, c, pack16<T>(ob));
             }
-            stage_put(sta, lane, c, pack16<T>(oa));
-            if constexpr (kMrgChains == 2) stage_put(stb, lane, c, pack16<T>(ob));
+            __syncwarp();
+            const uint64_t ea = w0 + rb + off;
+            mrg_store_tile<T>(sta, out + ea, seg, lane, ea, a.n, vec_ok);
+            if constexpr (kMrgChains == 2) mrg_store_tile<T>(stb, out + ea + half, seg, lane, ea + half, a.n, vec_ok);
+            __syncwarp();
         }
-        __syncwarp();
-        mrg_store_tile<T>(sta, out + warp_elem0 + off, a.chunk, lane, warp_elem0 + off, a.n, vec_ok);
-        if constexpr (kMrgChains == 2)
-            mrg_store_tile<T>(stb, out + warp_elem0 + half + off, a.chunk, lane, warp_elem0 + half + off, a.n,
-                              vec_ok);
-        __syncwarp();
+        if constexpr (MrgPlan<X>::kSegmented) {  // otherwise one round (seg = half / 32)
+            if (rb + 32 * seg < half) {
+                mrg_jump_state(a, sa);
+                if constexpr (kMrgChains == 2) mrg_jump_state(a, sb);
+            }
+        }
     }
 }
 
