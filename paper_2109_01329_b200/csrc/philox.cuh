@@ -102,6 +102,15 @@ __device__ __forceinline__ U4 funnel(const U4& a, const U4& b) {
 // Blocks per thread per pass on the aligned path: 4 for 4-byte outputs (two
 // 256-bit stores of 64 contiguous bytes), 2 for 8-byte outputs.
 template <typename T> struct PhiloxBpt { static constexpr int kValue = 4; };
+#ifndef PRNG_PHILOX_PIPE
+#define PRNG_PHILOX_PIPE 1
+#endif
+// Aligned-path software pipelining (Philox of pass i+1 next to the transform
+// of pass i) for the fast fp32 Box-Muller transforms.
+template <int X>
+constexpr bool philox_pipelined() {
+    return PRNG_PHILOX_PIPE && (X == kGaussF32Fast || X == kLognF32Fast);
+}
 template <> struct PhiloxBpt<double> { static constexpr int kValue = 2; };
 
 template <int X, int SHIFT>
@@ -117,6 +126,28 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
         const uint32_t gstep = gstride * BPT;
         const uint32_t gfull = a.ngroups - a.ngroups % BPT;
         T* dst = body + (size_t)4 * BPT * gtid;
+        if constexpr (philox_pipelined<X>()) {
+            // Software-pipelined: the next pass's Philox blocks (FMA-heavy
+            // IMAD.WIDE + ALU) are computed in the same basic block as this
+            // pass's transform (FMA-lite, XU, LSU), so the scheduler can
+            // interleave the two instruction mixes.  The blocks computed on
+            // the last pass are not used (counter wrap is harmless there).
+            U4 w[BPT];
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre(a.k0, a.k1, a.c0 + gtid * BPT + j, a.pre);
+            for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
+                U4 nw[BPT];
+#pragma unroll
+                for (int j = 0; j < BPT; ++j) nw[j] = philox_block_pre(a.k0, a.k1, a.c0 + g0 + gstep + j, a.pre);
+                T o[BPT][4];
+#pragma unroll
+                for (int j = 0; j < BPT; ++j) xform4<X>(w[j], a.p, o[j]);
+#pragma unroll
+                for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
+#pragma unroll
+                for (int j = 0; j < BPT; ++j) w[j] = nw[j];
+            }
+        } else
         for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
             T o[BPT][4];
 #pragma unroll
@@ -198,11 +229,14 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
 // kernels (C1/C4) a bound of 5 (4 for the funnel variants) lets ptxas use
 // ~48 registers and schedule the four blocks' multiply chains further
 // apart: occupancy 5 instead of 6 but +3.5-4% throughput (+6% for the
-// funnel), measured; the other transforms keep ptxas'
-// default (0 = no bound).  Eight blocks per thread measured 20% slower.
+// funnel), measured; the pipelined fast gaussian takes 4
+// (61 registers: +1.4% over no bound, 5 is 2.4% slower), the other
+// transforms keep ptxas' default (0 = no bound).  Eight blocks per thread measured 20% slower.
 template <int X, int SHIFT>
 constexpr int philox_min_blocks() {
-    return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? 5 : 4) : 0;
+    return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? 5 : 4)
+           : (X == kGaussF32Fast && philox_pipelined<X>() && SHIFT == 0) ? 4
+                                                                          : 0;
 }
 
 template <int X, int SHIFT>
