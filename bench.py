@@ -79,7 +79,14 @@ def make_spec(P, dist, prec):
 
 
 class ClockSampler:
-    """NVML sampling of SM clock and throttle reasons during the timed region."""
+    """NVML sampling of SM clock and throttle reasons during the timed region.
+
+    NVML's clock and event-reason readings trail the hardware by tens of ms
+    (a 200-launch series with nvidia-smi alongside, tools/launch_series.py,
+    profiles/r1_launch_series.txt, showed the headline kernel entering
+    sw_power_cap about 60 ms into a sustained run while short NVML samples
+    still read max clocks), so sampling continues for `tail` seconds after
+    the region; sm_min_mhz is reported next to the median."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
@@ -87,9 +94,10 @@ class ClockSampler:
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
 
-    def __init__(self, index, period=0.01):
+    def __init__(self, index, period=0.005, tail=0.15):
         self.samples, self.reasons, self.ok = [], 0, False
         self.period = period
+        self.tail = tail
         self._stop = threading.Event()
         try:
             import pynvml
@@ -121,6 +129,7 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         if self.ok:
+            time.sleep(self.tail)
             self._stop.set()
             self._t.join()
 
@@ -128,8 +137,9 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
         names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
-                "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_min_mhz": min(self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples),
+                "sampling": f"NVML every {self.period * 1e3:.0f} ms over the timed region + {self.tail * 1e3:.0f} ms tail"}
 
 
 def measured_peak():
