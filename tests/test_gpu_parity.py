@@ -203,6 +203,26 @@ def test_mrg_c2_full_size_spot_windows():
     assert float(v.min()) >= -123.456 and float(v.max()) < 987.654
 
 
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_mrg_segment_layout_edges_full_arrays(prec):
+    """Full-array equality with the sequential oracle around the MRG kernel's
+    layout boundaries: tiles (16/32 words), 512-byte lane segments and their
+    rounds (fp64 takes the segmented path with per-lane jumps), warp regions,
+    partial last warps and requests whose end falls inside the second chain."""
+    s1, s2 = O.seed_mrg(777)
+    base = P.seed_engine(MRG, 777)
+    nmax = (1 << 25) + 12345  # ~3 segment rounds (2 jumps) per chain at fp64
+    words = O.mrg_fill(*s1, *s2, nmax + 64)[0]
+    sizes = [1, 2, 15, 16, 17, 63, 64, 65, 127, 128, 129, 2047, 2048, 2049, 4095, 4097, 64 * 32 + 5,
+             128 * 32 - 1, 65536 + 3, 99991, (1 << 20) - 1, (1 << 21) + 4099, (1 << 24) + 77, nmax]
+    for skip in (0, 3):
+        for n in sizes:
+            st = P.skip_ahead(base, skip) if skip else base
+            _, got = P.generate(P.Uniform(-1.5, 2.25, prec), st, n)
+            want = O.range_transform(O.words_to_unit(words[skip:skip + n], prec), -1.5, 2.25)
+            assert np.array_equal(host(got), want), (prec, skip, n)
+
+
 # ----------------------------------------------------- large-size properties
 
 
