@@ -46,16 +46,19 @@ extern "C" {
 #define PRNG_ERR_VALUE (-4)              /* ValueError (engine.py:206,219) */
 #define PRNG_ERR_CUDA (-5)               /* CUDA runtime failure           */
 
-/* Gaussian / lognormal fp32 method.  FAST: fp32 logf/sqrtf/sincospif
+/* Gaussian / lognormal fp32 method.  FAST: fp32 SFU lg2/sqrt with a short
+ * series near u1 = 0 and a shared-memory sin/cos table with angle addition
  * (documented tolerance).  ACCURATE: the reference's
  * fp64 formula, then cast (fp64 outputs always use ACCURATE). */
 #define PRNG_METHOD_FAST 0
 #define PRNG_METHOD_ACCURATE 1
 /* Gaussian only (fp32 and fp64): bit-identical to the reference's fp64
- * Box-Muller (_core.pyx:116-121 with the host libm): log(u1') and
- * (sin t, cos t) are gathered from tables tabulated from the host libm over
- * their whole 2^24-point domains (built once per process, 384 MB per device;
- * prng_exact_tables_prepare builds them ahead of the first request). */
+ * Box-Muller (_core.pyx:116-121 with the host libm): the device
+ * approximations of log(u1') and (sin t, cos t) are corrected to the host
+ * libm's values by 4-bit ulp deltas tabulated over their whole 2^24-point
+ * domains (~24 MB per device plus short escape lists, built once per
+ * process; prng_exact_tables_prepare builds them ahead of the first
+ * request). */
 #define PRNG_METHOD_EXACT 2
 
 int prng_abi_version(void);

@@ -14,11 +14,13 @@ Results vs the reference:
   * uniform_bits, uniform fp32/fp64 on [a, b): bit-exact;
   * gaussian/lognormal fp64, and fp32 with method="accurate": fp64 math on
     the device (CUDA libdevice log/sincos/exp vs glibc), a few fp64 ulps;
-  * gaussian/lognormal fp32 with method="fast" (default): fp32 logf /
-    sqrtf / sincospif / expf, within the stated fp32 tolerance;
+  * gaussian/lognormal fp32 with method="fast" (default): fp32 SFU lg2 /
+    sqrt (series near u1 = 0), table-driven sin/cos, ex2, within the stated
+    fp32 tolerance;
   * gaussian fp32/fp64 with method="exact": bit-identical to the reference
-    (log / sin / cos gathered from tables of the host libm over their whole
-    2^24-point input domains, csrc/common.cuh box_muller_exact).
+    (device log / sin / cos corrected to the host libm by per-input ulp
+    deltas over their whole 2^24-point input domains, csrc/common.cuh
+    box_muller_exact).
 """
 
 from __future__ import annotations
