@@ -622,7 +622,7 @@ __global__ void box_muller_kernel(const double* u1, const double* u2, uint64_t m
 template <int X>
 __global__ void words_kernel(const uint32_t* __restrict__ w, uint64_t n, XformParams p,
                              typename XformTraits<X>::T* __restrict__ out) {
-    xform_prologue<X>();
+    xform_prologue<X>(p);
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;; i += stride) {
         if constexpr (XformTraits<X>::kPair) {

@@ -477,14 +477,24 @@ __device__ __forceinline__ float2* sincos_tab() {
     return tab;
 }
 
+// The fast gaussian's table holds (sin, cos) * stddev * sqrt(2 ln 2), so the
+// per-pair r scaling multiply disappears (one more rounding on the table:
+// exhaustive worst err/allowed 0.658 vs 0.669; +2% at 2^30).  The lognormal
+// keeps the unscaled table (measured 1% slower scaled).
+template <int X>
+constexpr bool bm_table_scaled() {
+    return X == kGaussF32Fast;
+}
+
 template <int X, int TL = kPhiloxTabLog2>
-__device__ __forceinline__ void xform_prologue() {
+__device__ __forceinline__ void xform_prologue(const XformParams& p) {
     if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
         float2* tab = sincos_tab<TL>();
+        const float S = bm_table_scaled<X>() ? p.scale_f * kBmRq : 1.0f;
         for (int i = threadIdx.x; i < (1 << TL); i += blockDim.x) {
             float sn, cs;
             sincospif((float)i * (2.0f / (1 << TL)), &sn, &cs);  // angle 2 pi i / 2^TL, exact argument
-            tab[i] = make_float2(sn, cs);
+            tab[i] = bm_table_scaled<X>() ? make_float2(sn * S, cs * S) : make_float2(sn, cs);
         }
         __syncthreads();
     }
@@ -499,13 +509,18 @@ __device__ __forceinline__ float neg_lg2_1mu(uint32_t w0) {
     if constexpr (PRNG_BM_SER_LOG2K == 0) {
         return -l2;
     } else {
-        const float x = kf * 5.9604644775390625e-08f;  // u1, exact
-        constexpr float c[5] = {1.4426950408889634f, 0.7213475204444817f, 0.48089834696298783f,
-                                0.36067376022224085f, 0.28853900817779266f};  // 1/(j ln 2)
+        // x (1 + x/2 + x^2/3 ...) / ln 2 with x = u1 = kf 2^-24, evaluated on kf
+        // with the coefficients pre-scaled by 2^(-24 (j + 1)): every
+        // intermediate is the x-form's value times a power of two, so the
+        // roundings (and the result) are identical, one multiply fewer.
+        constexpr float c[5] = {1.4426950408889634f * 0x1p-24f, 0.7213475204444817f * 0x1p-48f,
+                                0.48089834696298783f * 0x1p-72f, 0.36067376022224085f * 0x1p-96f,
+                                0.28853900817779266f * 0x1p-120f};  // 1/(j ln 2) 2^(-24 j)
+        static_assert(PRNG_BM_SER_TERMS <= 4, "the fifth scaled coefficient is near the fp32 normal limit");
         float p = c[PRNG_BM_SER_TERMS - 1];
 #pragma unroll
-        for (int j = PRNG_BM_SER_TERMS - 2; j >= 0; --j) p = fmaf(p, x, c[j]);
-        return k < (1u << PRNG_BM_SER_LOG2K) ? x * p : -l2;
+        for (int j = PRNG_BM_SER_TERMS - 2; j >= 0; --j) p = fmaf(p, kf, c[j]);
+        return k < (1u << PRNG_BM_SER_LOG2K) ? kf * p : -l2;
     }
 }
 
@@ -514,9 +529,12 @@ __device__ __forceinline__ void sincos_2pi_k24(uint32_t w1, float& sn, float& cs
     constexpr int L = 24 - TL;  // low bits of k = w1 >> 8 left to the polynomial
     static_assert(L >= 1 && L <= 15, "table size");
     const float2 t = sincos_tab<TL>()[w1 >> (32 - TL)];
-    // bits [8, 8 + L) of w1 -> mantissa bits [23 - L, 23)
-    const float f = __uint_as_float(((w1 << (15 - L)) & (((1u << L) - 1u) << (23 - L))) | 0x3F800000u);
-    constexpr float C = 3.7450702e-07f * (float)(1u << L);  // 2 pi 2^(L - 24) (power-of-two scaling of 2 pi 2^-24)
+    // bits [8, 8 + L) of w1 stay where they are, as mantissa bits [8, 8 + L)
+    // under the exponent of 1.0f (one LOP3, no shift): f - 1 = low * 2^-15.
+    uint32_t fb;  // (w1 & mask) | bits(1.0f) as ONE 3-input LOP3 (one operand in a register)
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(fb) : "r"(w1), "n"(((1u << L) - 1u) << 8), "r"(0x3F800000u));
+    const float f = __uint_as_float(fb);
+    constexpr float C = 3.7450702e-07f * 32768.0f;  // 2 pi 2^-9 (power-of-two scaling of 2 pi 2^-24)
     const float x = fmaf(f, C, -C);
     if constexpr (TL < PRNG_BM_COS_QUAD_BELOW) {
         const float cl = fmaf(x * x, -0.5f, 1.0f);
@@ -629,7 +647,8 @@ __device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformPar
     if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
         float rq, sn, cs;
         box_muller_f32_parts<TL>(w0, w1, rq, sn, cs);
-        const float rs = rq * (p.scale_f * kBmRq);  // stddev and sqrt(2 ln 2) folded into r (loop-invariant)
+        // stddev and sqrt(2 ln 2) folded into r (loop-invariant) or into the table
+        const float rs = bm_table_scaled<X>() ? rq : rq * (p.scale_f * kBmRq);
         if constexpr (X == kGaussF32Fast) {
             o0 = fmaf(rs, cs, p.off_f);
             o1 = fmaf(rs, sn, p.off_f);

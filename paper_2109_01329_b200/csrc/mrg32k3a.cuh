@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
         sj1[i] = a.j1[i / 9][i % 9];
         sj2[i] = a.j2[i / 9][i % 9];
     }
-    xform_prologue<X, kMrgTabLog2>();
+    xform_prologue<X, kMrgTabLog2>(a.p);
     __syncthreads();
 
     const uint32_t lane = threadIdx.x & 31;

@@ -241,7 +241,7 @@ constexpr int philox_min_blocks() {
 
 template <int X, int SHIFT>
 __global__ void __launch_bounds__(kPhiloxThreads, philox_min_blocks<X, SHIFT>()) philox_kernel(const PhiloxBody a) {
-    xform_prologue<X>();
+    xform_prologue<X>(a.p);
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gstride = gridDim.x * blockDim.x;
     if (a.s.n) {
