@@ -479,18 +479,22 @@ __device__ __forceinline__ float2* sincos_tab() {
 
 // The fast gaussian's table holds (sin, cos) * stddev * sqrt(2 ln 2), so the
 // per-pair r scaling multiply disappears (one more rounding on the table:
-// exhaustive worst err/allowed 0.658 vs 0.669; +2% at 2^30).  The lognormal
-// keeps the unscaled table (measured 1% slower scaled).
+// exhaustive worst err/allowed 0.658 vs 0.669; +2% at 2^30); the lognormal's
+// also folds log2(e), removing the exp's argument multiplies.
 template <int X>
 constexpr bool bm_table_scaled() {
-    return X == kGaussF32Fast;
+    return X == kGaussF32Fast || X == kLognF32Fast;
 }
+constexpr float kLog2E = 1.4426950408889634f;
 
 template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform_prologue(const XformParams& p) {
     if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
         float2* tab = sincos_tab<TL>();
-        const float S = bm_table_scaled<X>() ? p.scale_f * kBmRq : 1.0f;
+        // lognormal: also log2(e), so exp(m + s z) = ex2(fma(rq, cs', m log2(e)))
+        const float S = !bm_table_scaled<X>() ? 1.0f
+                        : X == kLognF32Fast   ? p.scale_f * kBmRq * kLog2E
+                                              : p.scale_f * kBmRq;
         for (int i = threadIdx.x; i < (1 << TL); i += blockDim.x) {
             float sn, cs;
             sincospif((float)i * (2.0f / (1 << TL)), &sn, &cs);  // angle 2 pi i / 2^TL, exact argument
@@ -653,8 +657,14 @@ __device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformPar
             o0 = fmaf(rs, cs, p.off_f);
             o1 = fmaf(rs, sn, p.off_f);
         } else {
-            o0 = fmaf(__expf(fmaf(rs, cs, p.off_f)), p.ln_scale_f, p.ln_displ_f);  // ex2.approx: 2^-21 rel
-            o1 = fmaf(__expf(fmaf(rs, sn, p.off_f)), p.ln_scale_f, p.ln_displ_f);
+            // table scaled by s sqrt(2 ln 2) log2(e): the exponent in base 2 is one
+            // FMA; ex2.approx (~2^-22 rel)
+            const float off2 = p.off_f * kLog2E;  // loop-invariant
+            float e0, e1;
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(fmaf(rs, cs, off2)));
+            asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(fmaf(rs, sn, off2)));
+            o0 = fmaf(e0, p.ln_scale_f, p.ln_displ_f);
+            o1 = fmaf(e1, p.ln_scale_f, p.ln_displ_f);
         }
     } else {
         xform2<X>(w0, w1, p, o0, o1);
