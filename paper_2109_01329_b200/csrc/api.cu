@@ -482,11 +482,11 @@ int check_mrg_state(const uint32_t* s1, const uint32_t* s2) {
 struct MrgTables {
     uint32_t nbits;
     uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];  // A^(seg * 2^b)
-    uint32_t h1[9], h2[9];                              // A^(32*chunk/kMrgChains)
+    uint32_t h1[9], h2[9];                              // A^(32*chunk/chains)
     MrgJump b1, b2;                                     // A^(31*seg), split
 };
 std::mutex g_mrg_mu;
-std::map<std::tuple<uint64_t, uint64_t, uint32_t>, MrgTables> g_mrg_tables;
+std::map<std::tuple<uint64_t, uint64_t, uint32_t, uint64_t>, MrgTables> g_mrg_tables;
 
 // B = hi*2^16 + lo with B's entries as symmetric residues mod m.
 MrgJump split_jump(const Mat3& b, uint64_t m) {
@@ -502,15 +502,15 @@ MrgJump split_jump(const Mat3& b, uint64_t m) {
 
 // Returned by value: another thread may evict the cache entry right after
 // the lock is released.
-MrgTables mrg_tables(uint64_t chunk, uint64_t seg, uint32_t nbits) {
+MrgTables mrg_tables(uint64_t chunk, uint64_t seg, uint32_t nbits, uint64_t chains) {
     std::lock_guard<std::mutex> lk(g_mrg_mu);
-    auto key = std::make_tuple(chunk, seg, nbits);
+    auto key = std::make_tuple(chunk, seg, nbits, chains);
     auto it = g_mrg_tables.find(key);
     if (it != g_mrg_tables.end()) return it->second;
     MrgTables t{};
     t.nbits = nbits;
     Mat3 a, b;
-    mat_pow_u64(32 * chunk / kMrgChains, &a, &b);
+    mat_pow_u64(32 * chunk / chains, &a, &b);
     for (int e = 0; e < 9; ++e) {
         t.h1[e] = (uint32_t)a.v[e];
         t.h2[e] = (uint32_t)b.v[e];
@@ -549,18 +549,19 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     if (rc) return rc;
     // A lane's share `chunk` is a whole number of segments per chain, so
     // every chain region is whole rounds (MrgPlan: segments of 4 tiles, or
-    // one segment of chunk / kMrgChains words).
+    // one segment of chunk / kChains words).
     const uint64_t tmax = (uint64_t)sms * occ * kMrgThreads;
     uint64_t chunk = (n + tmax - 1) / tmax;
-    const uint64_t unit = MrgPlan<X>::kSegmented ? kMrgChains * 4 * TW : kMrgChains * TW;
+    constexpr uint64_t NC = MrgPlan<X>::kChains;
+    const uint64_t unit = MrgPlan<X>::kSegmented ? NC * 4 * TW : NC * TW;
     chunk = (chunk + unit - 1) / unit * unit;
-    const uint64_t seg = MrgPlan<X>::kSegmented ? 4 * TW : chunk / kMrgChains;
+    const uint64_t seg = MrgPlan<X>::kSegmented ? 4 * TW : chunk / NC;
     const uint64_t tact = (n + chunk - 1) / chunk;
     const uint64_t qmax = ((tact - 1) / 32) * 32 * chunk / seg + 31;  // last lane's first segment
     uint32_t nbits = 0;
     while (nbits < 64 && (qmax >> nbits) != 0) ++nbits;
     if (nbits > (uint32_t)kMrgMaxBits) return fail(PRNG_ERR_INVALID_PARAMETER, "request too large");
-    const MrgTables tb = mrg_tables(chunk, seg, nbits);
+    const MrgTables tb = mrg_tables(chunk, seg, nbits, NC);
     MrgLaunch a{};
     for (int i = 0; i < 3; ++i) {
         a.s1[i] = s1[i];

@@ -6,8 +6,8 @@
 // engine.py:201-202).
 //
 // Layout ("segmented rows").  Warp w owns the region [w*32*chunk,
-// (w+1)*32*chunk) of the request, cut into kMrgChains halves, one per
-// interleaved recurrence ("chain") of every lane.  A chain's half is walked
+// (w+1)*32*chunk) of the request, cut into kChains regions, one per
+// interleaved recurrence ("chain") of every lane.  A chain's region is walked
 // in rounds of 32 segments of `seg` words (seg = 4 tiles = 512 bytes of
 // output for the plain fp64 transforms, MrgPlan); in each round lane L produces the segment [round*32*seg + L*seg,
 // +seg) and then jumps its state 31*seg words ahead (x -> B x mod m, B =
@@ -20,8 +20,8 @@
 //
 // Lane start states are A^(q*seg) s0 with q = (region start)/seg + L,
 // assembled from host tables J_b = A^(seg*2^b) staged in shared memory (one
-// 3x3 mod-m mat-vec per set bit of q); the second chain starts from the
-// first by the host matrix A^(32*chunk/kMrgChains).  Each 128-byte tile of
+// 3x3 mod-m mat-vec per set bit of q); each further chain starts from the
+// previous one by the host matrix A^(32*chunk/kChains).  Each 128-byte tile of
 // every segment is transposed through an XOR-swizzled shared-memory stage
 // (16-byte chunks) so each 128-bit store instruction writes four segments'
 // whole 128-byte lines.
@@ -36,21 +36,25 @@ constexpr int kMrgThreads = 128;
 #ifndef PRNG_MRG_MINB
 #define PRNG_MRG_MINB 6
 #endif
-#ifndef PRNG_MRG_CHAINS
-#define PRNG_MRG_CHAINS 2
+#ifndef PRNG_MRG_SEG_CHAINS
+#define PRNG_MRG_SEG_CHAINS 2
 #endif
-constexpr int kMrgChains = PRNG_MRG_CHAINS;  // interleaved recurrences per thread (1 or 2)
+#ifndef PRNG_MRG_SEG_MINB
+#define PRNG_MRG_SEG_MINB 4
+#endif
 
 // Segmented rows (seg = 4 tiles, a jump every seg words) pay off where the
 // store pattern is the bound: the plain 8-byte transforms.  Elsewhere (4-byte
 // outputs at <= 3.6 TB/s, the Box-Muller transforms) the jumps cost more than
-// the pattern, and seg = chunk / kMrgChains gives one round per lane (no
-// jumps).  The 8-byte kernels take a 5-CTA bound (no spills with the jump
-// temporaries), the others 6.
+// the pattern, and seg = chunk / kChains gives one round per lane (no
+// jumps).  kChains interleaved recurrences per lane; the 8-byte kernels take
+// a 4-CTA bound (128 registers: no spills with the jump temporaries; 5 CTAs
+// spilled 12 bytes and ran 2-5% slower), the others 6.
 template <int X>
 struct MrgPlan {
     static constexpr bool kSegmented = sizeof(typename XformTraits<X>::T) == 8 && !XformTraits<X>::kPair;
-    static constexpr int kMinBlocks = kSegmented ? PRNG_MRG_MINB - 1 : PRNG_MRG_MINB;
+    static constexpr int kChains = kSegmented ? PRNG_MRG_SEG_CHAINS : 2;
+    static constexpr int kMinBlocks = kSegmented ? PRNG_MRG_SEG_MINB : PRNG_MRG_MINB;
 };
 
 // Jump matrix B (entries as symmetric residues) split as B = hi*2^16 + lo,
@@ -63,12 +67,12 @@ struct MrgJump {
 struct MrgLaunch {
     uint32_t s1[3], s2[3];
     uint64_t n;
-    uint64_t chunk;  // words per lane (region of a warp = 32*chunk; multiple of kMrgChains*seg)
+    uint64_t chunk;  // words per lane (region of a warp = 32*chunk; multiple of kChains*seg)
     uint64_t seg;    // words per lane segment (4 tiles)
     uint32_t nbits;
     uint32_t j1[kMrgMaxBits][9];  // A^(seg * 2^b)
     uint32_t j2[kMrgMaxBits][9];
-    uint32_t h1[9], h2[9];  // A^(32*chunk/kMrgChains): chain 0 -> chain 1
+    uint32_t h1[9], h2[9];  // A^(32*chunk/kChains): chain c -> chain c+1
     MrgJump b1, b2;         // A^(31*seg): end of a segment -> start of the lane's next one
     void* out;
     XformParams p;
@@ -171,7 +175,8 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
     using T = typename XformTraits<X>::T;
     constexpr int TW = MrgTile<T>::kWords;
     constexpr int WARPS = kMrgThreads / 32;
-    __shared__ uint4 stage[kMrgChains][WARPS][32 * 8];
+    constexpr int NC = MrgPlan<X>::kChains;
+    __shared__ uint4 stage[NC][WARPS][32 * 8];
     __shared__ uint32_t sj1[kMrgMaxBits * 9], sj2[kMrgMaxBits * 9];
 
     for (uint32_t i = threadIdx.x; i < a.nbits * 9; i += blockDim.x) {
@@ -195,61 +200,59 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
             mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
         }
     }
-    MrgStateF64 sa{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
-                   mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
-    MrgStateF64 sb = sa;
-    if constexpr (kMrgChains == 2) {
-        mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
-        mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
-        sb = MrgStateF64{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
-                         mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
+    MrgStateF64 st[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c) {  // chain c starts one chain region (A^(32 chunk / NC)) after chain c-1
+            mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
+            mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
+        }
+        st[c] = MrgStateF64{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
+                            mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
     }
 
-    const uint64_t half = 32 * a.chunk / kMrgChains;  // words per chain region
+    const uint64_t region = 32 * a.chunk / NC;  // words per chain region
     const uint64_t seg = a.seg;
     T* __restrict__ out = static_cast<T*>(a.out);
-    uint4* sta = stage[0][warp];
-    uint4* stb = stage[kMrgChains - 1][warp];
     const bool vec_ok = ((uintptr_t)out & 15u) == 0;
     constexpr int CE = 16 / sizeof(T);  // elements per 16-byte chunk
-    for (uint64_t rb = 0; rb < half; rb += 32 * seg) {
+    for (uint64_t rb = 0; rb < region; rb += 32 * seg) {
         if (w0 + rb >= a.n) break;  // warp-uniform
         for (uint64_t off = 0; off < seg; off += TW) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                T oa[CE], ob[CE];
+                T o[NC][CE];
                 if constexpr (XformTraits<X>::kPair) {
 #pragma unroll
                     for (int k = 0; k < CE; k += 2) {
-                        const uint32_t a0 = mrg_step_f64(sa);
-                        const uint32_t a1 = mrg_step_f64(sa);
-                        xform2k<X, kMrgTabLog2>(a0, a1, a.p, oa[k], oa[k + 1]);
-                        if constexpr (kMrgChains == 2) {
-                            const uint32_t b0 = mrg_step_f64(sb);
-                            const uint32_t b1 = mrg_step_f64(sb);
-                            xform2k<X, kMrgTabLog2>(b0, b1, a.p, ob[k], ob[k + 1]);
+#pragma unroll
+                        for (int h = 0; h < NC; ++h) {
+                            const uint32_t u0 = mrg_step_f64(st[h]);
+                            const uint32_t u1 = mrg_step_f64(st[h]);
+                            xform2k<X, kMrgTabLog2>(u0, u1, a.p, o[h][k], o[h][k + 1]);
                         }
                     }
                 } else {
 #pragma unroll
                     for (int k = 0; k < CE; ++k) {
-                        oa[k] = xform1<X>(mrg_step_f64(sa), a.p);
-                        if constexpr (kMrgChains == 2) ob[k] = xform1<X>(mrg_step_f64(sb), a.p);
+#pragma unroll
+                        for (int h = 0; h < NC; ++h) o[h][k] = xform1<X>(mrg_step_f64(st[h]), a.p);
                     }
                 }
-                stage_put(sta, lane, c, pack16<T>(oa));
-                if constexpr (kMrgChains == 2) stage_put(stb, lane, c, pack16<T>(ob));
+#pragma unroll
+                for (int h = 0; h < NC; ++h) stage_put(stage[h][warp], lane, c, pack16<T>(o[h]));
             }
             __syncwarp();
             const uint64_t ea = w0 + rb + off;
-            mrg_store_tile<T>(sta, out + ea, seg, lane, ea, a.n, vec_ok);
-            if constexpr (kMrgChains == 2) mrg_store_tile<T>(stb, out + ea + half, seg, lane, ea + half, a.n, vec_ok);
+#pragma unroll
+            for (int h = 0; h < NC; ++h)
+                mrg_store_tile<T>(stage[h][warp], out + ea + h * region, seg, lane, ea + h * region, a.n, vec_ok);
             __syncwarp();
         }
-        if constexpr (MrgPlan<X>::kSegmented) {  // otherwise one round (seg = half / 32)
-            if (rb + 32 * seg < half) {
-                mrg_jump_state(a, sa);
-                if constexpr (kMrgChains == 2) mrg_jump_state(a, sb);
+        if constexpr (MrgPlan<X>::kSegmented) {  // otherwise one round (seg = region / 32)
+            if (rb + 32 * seg < region) {
+#pragma unroll
+                for (int h = 0; h < NC; ++h) mrg_jump_state(a, st[h]);
             }
         }
     }
