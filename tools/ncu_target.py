@@ -19,6 +19,7 @@ W = {
     "logn_f32": ("philox", lambda: P.Lognormal(), torch.float32),
     "mrg_bits": ("mrg", lambda: P.UniformBits(), torch.uint32),
     "mrg_f64": ("mrg", lambda: P.Uniform(-1.0, 1.0, "fp64"), torch.float64),
+    "mrg_f32": ("mrg", lambda: P.Uniform(-1.0, 1.0), torch.float32),
     "fill": (None, None, torch.float32),
 }
 
