@@ -65,7 +65,9 @@ struct PhiloxPre {
     uint32_t r2_x3;  // hi(M0 U0) ^ (k1 + W1)        (round 2: c2'' = lo(M0 c0) ^ r2_x3)
     uint32_t r2_c3;  // lo(M0 U0), U0 = hi(M1 c2) ^ c1 ^ k0
     uint32_t r3_x3;  // r2_c3 ^ (k1 + 2 W1)
+    uint32_t rk0[8], rk1[8];  // round keys k + i W for rounds i = 2..9 (kernel-parameter operands)
 };
+
 
 __host__ __device__ inline PhiloxPre philox_pre(uint32_t k0, uint32_t k1, uint32_t c1, uint32_t c2, uint32_t c3) {
     const uint64_t p1 = (uint64_t)kPhiloxM1 * c2;
@@ -78,10 +80,19 @@ __host__ __device__ inline PhiloxPre philox_pre(uint32_t k0, uint32_t k1, uint32
     q.r2_x3 = (uint32_t)(p0u >> 32) ^ (k1 + kPhiloxW1);
     q.r2_c3 = (uint32_t)p0u;
     q.r3_x3 = q.r2_c3 ^ (k1 + 2 * kPhiloxW1);
+    for (int i = 0; i < 8; ++i) {
+        q.rk0[i] = k0 + (uint32_t)(i + 2) * kPhiloxW0;
+        q.rk1[i] = k1 + (uint32_t)(i + 2) * kPhiloxW1;
+    }
     return q;
 }
 
 // Philox4x32-10 of counter (c0, c1, c2, c3) given philox_pre(k0, k1, c1, c2, c3).
+// RK: take the round keys from q's table -- constant-bank operands of the
+// LOP3s when q is a kernel parameter (no per-pass key arithmetic: -12 of 225
+// instructions per 16 fp32 uniforms, +2-3%; measured neutral-to-worse for
+// the bits and Box-Muller kernels, which recompute them).
+template <bool RK = false>
 __device__ __forceinline__ U4 philox_block_pre(uint32_t k0, uint32_t k1, uint32_t c0, const PhiloxPre& q) {
     uint64_t p0 = (uint64_t)kPhiloxM0 * c0;  // round 1
     const uint32_t x2 = (uint32_t)(p0 >> 32) ^ q.r1_x3;
@@ -92,22 +103,20 @@ __device__ __forceinline__ U4 philox_block_pre(uint32_t k0, uint32_t k1, uint32_
     const uint32_t y2 = x3 ^ q.r2_x3;
     p0 = (uint64_t)kPhiloxM0 * y0;  // round 3
     p1 = (uint64_t)kPhiloxM1 * y2;
-    U4 c{(uint32_t)(p1 >> 32) ^ y1 ^ (k0 + 2 * kPhiloxW0), (uint32_t)p1, (uint32_t)(p0 >> 32) ^ q.r3_x3,
-         (uint32_t)p0};
-    k0 += 3 * kPhiloxW0;
-    k1 += 3 * kPhiloxW1;
+    U4 c{(uint32_t)(p1 >> 32) ^ y1 ^ (RK ? q.rk0[0] : k0 + 2 * kPhiloxW0), (uint32_t)p1,
+         (uint32_t)(p0 >> 32) ^ q.r3_x3, (uint32_t)p0};
 #pragma unroll
     for (int i = 3; i < 10; ++i) {
+        const uint32_t ki0 = RK ? q.rk0[i - 2] : k0 + (uint32_t)i * kPhiloxW0;
+        const uint32_t ki1 = RK ? q.rk1[i - 2] : k1 + (uint32_t)i * kPhiloxW1;
         const uint64_t a = (uint64_t)kPhiloxM0 * c.x;
         const uint64_t b = (uint64_t)kPhiloxM1 * c.z;
-        const uint32_t t0 = (uint32_t)(b >> 32) ^ c.y ^ k0;
-        const uint32_t t2 = (uint32_t)(a >> 32) ^ c.w ^ k1;
+        const uint32_t t0 = (uint32_t)(b >> 32) ^ c.y ^ ki0;
+        const uint32_t t2 = (uint32_t)(a >> 32) ^ c.w ^ ki1;
         c.y = (uint32_t)b;
         c.w = (uint32_t)a;
         c.x = t0;
         c.z = t2;
-        k0 += kPhiloxW0;
-        k1 += kPhiloxW1;
     }
     return c;
 }

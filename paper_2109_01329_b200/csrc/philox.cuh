@@ -102,6 +102,12 @@ __device__ __forceinline__ U4 funnel(const U4& a, const U4& b) {
 // Blocks per thread per pass on the aligned path: 4 for 4-byte outputs (two
 // 256-bit stores of 64 contiguous bytes), 2 for 8-byte outputs.
 template <typename T> struct PhiloxBpt { static constexpr int kValue = 4; };
+// Round keys from the parameter table (philox_block_pre<true>) for the
+// uniform transforms.
+template <int X>
+constexpr bool philox_rk() {
+    return X == kUnitF32 || X == kUniformF32 || X == kUnitF64 || X == kUniformF64;
+}
 #ifndef PRNG_PHILOX_PIPE
 #define PRNG_PHILOX_PIPE 1
 #endif
@@ -152,7 +158,7 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             T o[BPT][4];
 #pragma unroll
             for (int j = 0; j < BPT; ++j) {
-                const U4 w = philox_block_pre(a.k0, a.k1, a.c0 + g0 + j, a.pre);
+                const U4 w = philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + g0 + j, a.pre);
                 xform4<X>(w, a.p, o[j]);
             }
             if constexpr (sizeof(T) == 4) {
@@ -166,7 +172,7 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
         if (gtid == gstride - 1) {
             for (uint32_t g = gfull; g < a.ngroups; ++g) {
                 T o[4];
-                xform4<X>(philox_block_pre(a.k0, a.k1, a.c0 + g, a.pre), a.p, o);
+                xform4<X>(philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + g, a.pre), a.p, o);
                 st_group(body + (size_t)4 * g, o);
             }
         }
@@ -190,7 +196,7 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             U4 w[BPT + 1];
             if ((uint64_t)gb + BPT <= lim) {
 #pragma unroll
-                for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre(a.k0, a.k1, a.c0 + gb + j, a.pre);
+                for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + gb + j, a.pre);
             } else {
 #pragma unroll
                 for (int j = 0; j < BPT; ++j) {
