@@ -143,39 +143,6 @@ __device__ __forceinline__ uint32_t fold_mod(uint64_t t) {
     return (uint32_t)(t >= M ? t - M : t);
 }
 
-// One MRG32k3a step (_core.pyx:85-101), returning z = (p1 - p2) mod m1.
-// Mixed-pipe formulation: component 1 in 64-bit integer arithmetic on the
-// FMA-heavy pipe's IMAD.WIDE (signed products offset by 2^20*m1 to stay
-// unsigned: a12*x11 - a13n*x10 + 2^20*m1 is in [0, 2^53.3)), component 2 in
-// exact fp64 arithmetic on the FP64 pipe (L'Ecuyer's floating-point formulation), so the two halves of a
-// step run on different execution units.  All fp64 values are integers
-// below 2^53, every operation is exact:
-//   p = a21*x22 - a23n*x20          (|p| < 2^52.4: DMUL + DFMA, exact)
-//   k = rint(p / m2)                (DFMA with 1/m2 + 1.5*2^52 magic)
-//   p = p - k*m2  in (-m2, m2)      (DFMA, exact), + m2 if negative.
-struct MrgStateMixed {
-    uint32_t x10, x11, x12;
-    double y20, y21, y22;
-};
-
-__device__ __forceinline__ uint32_t mrg_step_mixed(MrgStateMixed& s) {
-    // t < 2^53.3, so one fold leaves t' = hi*209 + lo < 2^32 + 2^29.1 < 2 m1:
-    // a single conditional subtract finishes the reduction.
-    const uint64_t t = (uint64_t)kMrgA12 * s.x11 + (((uint64_t)kMrgM1 << 20) - (uint64_t)kMrgA13N * s.x10);
-    const uint64_t t1 = (t >> 32) * kMrgC1 + (t & 0xffffffffull);
-    const uint32_t p1 = (uint32_t)(t1 >= kMrgM1 ? t1 - kMrgM1 : t1);
-    constexpr double kMagic = 6755399441055744.0;  // 1.5 * 2^52
-    double p = __dmul_rn((double)kMrgA21, s.y22);
-    p = __fma_rn(-(double)kMrgA23N, s.y20, p);
-    const double k = __dadd_rn(__fma_rn(p, 1.0 / (double)kMrgM2, kMagic), -kMagic);
-    p = __fma_rn(-k, (double)kMrgM2, p);
-    p = p < 0.0 ? __dadd_rn(p, (double)kMrgM2) : p;
-    const uint32_t p2 = (uint32_t)__double2loint(__dadd_rn(p, 4503599627370496.0));  // + 2^52: low word = p
-    s.x10 = s.x11; s.x11 = s.x12; s.x12 = p1;
-    s.y20 = s.y21; s.y21 = s.y22; s.y22 = p;
-    return p1 >= p2 ? p1 - p2 : p1 - p2 + kMrgM1;
-}
-
 // All-fp64 formulation (L'Ecuyer's floating-point MRG32k3a with symmetric
 // residues).  Each component keeps its window as integers in [-m/2 - 1,
 // m/2 + 1] held in doubles, so a*x_i - b*x_j stays below 2^52.1 and is exact
