@@ -20,6 +20,8 @@ for st in (ph, mr):
                  P.Lognormal(), P.Lognormal(0.1, 0.3, 0.0, 1.0, "fp64")):
         for n in (1, 37, 4099, 100003):
             P.generate(spec, st, n)
+# MRG fp64 segmented path with several rounds (per-lane jumps) per chain
+P.generate(P.Uniform(-1.0, 2.0, "fp64"), mr, (1 << 25) + 12345)
 w = P.generate_words(ph, 1002)[1]
 P.gaussian_from_words(w, 0.0, 1.0, 1001)
 P.words_to_unit(w, "fp64")
