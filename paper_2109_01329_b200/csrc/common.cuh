@@ -429,8 +429,8 @@ __device__ __forceinline__ double corrected(double approx, int d, const ExactCor
 //    sincospif) for the top TL bits of k, and for the remaining
 //    x < 2 pi 2^-TL: sin x = x, cos x = 1 - x^2/2 (TL < 12) or 1 (TL >= 12:
 //    relative error x^2/2 <= 1.2e-6 on z, inside the 2^-19 tolerance).  x is
-//    built without I2FP: f = bits(0x3F800000 | low bits of k at the top of
-//    the mantissa) = 1 + klow 2^-L, x = (f - 1) C, one FFMA, exact input.
+//    built without I2FP or a shift: f = bits(0x3F800000 | (w1 & low-bit
+//    mask)) = 1 + klow 2^-15 (one LOP3), x = (f - 1) 2 pi 2^-9, one FFMA.
 #ifndef PRNG_BM_TAB_LOG2
 #define PRNG_BM_TAB_LOG2 12
 #endif
