@@ -101,7 +101,13 @@ __device__ __forceinline__ U4 funnel(const U4& a, const U4& b) {
 
 // Blocks per thread per pass on the aligned path: 4 for 4-byte outputs (two
 // 256-bit stores of 64 contiguous bytes), 2 for 8-byte outputs.
-template <typename T> struct PhiloxBpt { static constexpr int kValue = 4; };
+#ifndef PRNG_PHILOX_BPT
+#define PRNG_PHILOX_BPT 4
+#endif
+#ifndef PRNG_UNIT_MINB
+#define PRNG_UNIT_MINB 5
+#endif
+template <typename T> struct PhiloxBpt { static constexpr int kValue = PRNG_PHILOX_BPT; };
 // Round keys from the parameter table (philox_block_pre<true>) for the
 // uniform transforms.
 template <int X>
@@ -240,7 +246,7 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
 // transforms keep ptxas' default (0 = no bound).  Eight blocks per thread measured 20% slower.
 template <int X, int SHIFT>
 constexpr int philox_min_blocks() {
-    return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? 5 : 4)
+    return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? PRNG_UNIT_MINB : 4)
            : (X == kGaussF32Fast && philox_pipelined<X>() && SHIFT == 0) ? 4
                                                                           : 0;
 }
