@@ -583,3 +583,34 @@ def test_lognormal_fast_dense_stream(m, s, displ, scale):
         4 * np.spacing(np.abs(want)).astype(np.float64)
     err, exact = check_close(host(got), want, allowed, f"logn fast {m},{s}")
     print(f"lognormal fast ({m}, {s}, {displ}, {scale}): max abs err {err:.3e}, bit-exact {exact:.4f}")
+
+
+def test_integration_md_ctypes_stub_runs():
+    """The reference-side ctypes module printed in INTEGRATION.md §1 (what a
+    maintainer would add as portarng/_kernels/_cuda.py), executed verbatim
+    against the in-tree libprng_b200.so, returns the oracle's results."""
+    import os
+    import re
+    import types
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    text = (root / "INTEGRATION.md").read_text()
+    code = re.search(r"```python\n(# portarng/_kernels/_cuda\.py.*?)```", text, re.S).group(1)
+    os.environ.setdefault("PRNG_B200_LIB", str(P._lib.LIB_PATH))
+    mod = types.ModuleType("portarng_kernels_cuda")
+    exec(compile(code, "INTEGRATION.md:_cuda.py", "exec"), mod.__dict__)
+    assert mod.IMPL == "cuda"
+    key = O.seed_philox(777)
+    got = mod.philox_fill(key[0], key[1], 0xFFFFFFFF, 0xFFFFFFFF, 0, 0, 3, 4097)  # carry into lane 2
+    assert got.dtype == np.uint32 and np.array_equal(got, O.philox_words(key, 4 * (2**64 - 1) + 3, 4097))
+    s1, s2 = O.seed_mrg(777)
+    w, o1, o2 = mod.mrg_fill(*s1, *s2, 10007)
+    want, w1, w2 = O.mrg_fill(*s1, *s2, 10007)
+    assert np.array_equal(w, want) and tuple(o1) == tuple(w1) and tuple(o2) == tuple(w2)
+    u1 = (np.arange(1, 1001, dtype=np.float64) * 2.0**-24)
+    u2 = (np.arange(1000, dtype=np.float64) * 7 * 2.0**-24)
+    z0, z1 = mod.box_muller(u1, u2)
+    r0, r1 = O.box_muller(u1, u2)
+    assert np.array_equal(z0, r0) and np.array_equal(z1, r1)
+    assert mod.philox_fill(1, 2, 0, 0, 0, 0, 0, 0).shape == (0,)
