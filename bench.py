@@ -170,17 +170,39 @@ def metric_for(workload):
     return "Gsamples/s (and % HBM-write roofline) for " + WORKLOADS[workload][4]
 
 
-def cpu_baseline_sample(n_cpu, dist="uniform"):
+def cpu_baseline_sample(n_cpu, workload="c4"):
+    """The reference's CPU path for the workload, on a bounded sample (the
+    oracle/_ref core; MRG32k3a single-threaded: unsplittable in the
+    reference, rngburn.py:123)."""
+    import numpy as np
+
     from oracle.cpu_baseline import CpuPath
 
+    engine, dist, prec, _, _ = WORKLOADS[workload]
+    if engine == "mrg":
+        c = CpuPath(workers=1)
+        n_cpu = min(n_cpu, 1 << 24)
+        try:
+            best = c.time_cycle(lambda: c.burn_mrg_uniform((777,) * 3, (777,) * 3, n_cpu, -1.0, 1.0, prec))
+        finally:
+            c.close()
+        return {"value": n_cpu / best / 1e9, "unit": "Gsamples/s", "cores": 1, "kind": c.kind,
+                "sample": f"mrg32k3a seed 777 uniform {prec} [-1,1), n={n_cpu} per cycle, best of 3, one thread "
+                          "(_core.mrg_fill + words_to_unit + range_transform)"}
     c = CpuPath()
     try:
-        best, _ = c.time_philox_uniform(n_cpu, reps=3)
+        if dist == "gaussian":
+            n_cpu = min(n_cpu, 1 << 25)
+            out = np.empty(n_cpu, dtype=np.float32)
+            best = c.time_cycle(lambda: c.burn_philox_gaussian((777, 0), 0, n_cpu, out=out))
+            what = f"philox gaussian fp32 (0,1) seed 777, n={n_cpu} per cycle (_core.box_muller)"
+        else:
+            best, _ = c.time_philox_uniform(n_cpu, reps=3)
+            what = f"philox uniform fp32 [0,1) seed 777, n={n_cpu} per cycle"
     finally:
         c.close()
     return {"value": n_cpu / best / 1e9, "unit": "Gsamples/s", "cores": c.workers, "kind": c.kind,
-            "sample": f"philox uniform fp32 [0,1) seed 777, n={n_cpu} per cycle, best of 3, "
-                      f"burn_once-style chunked threads={c.workers}"}
+            "sample": f"{what}, best of 3, burn_once-style chunked threads={c.workers}"}
 
 
 def run_reference(args):
@@ -541,8 +563,8 @@ def run_ours(args):
         del host
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline_sample(args.cpu_n)
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload in ("c1", "c2", "c3_gauss", "c4"):
+        cpu = cpu_baseline_sample(args.cpu_n, args.workload)
 
     sweep = None
     if args.sweep:

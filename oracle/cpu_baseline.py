@@ -71,6 +71,48 @@ class CpuPath:
         w = self._mrg_fill(s1, s2, n)
         return O.range_transform(O.words_to_unit(w, precision), lo, hi)
 
+    def _box_muller(self, u1, u2):
+        if self.core is not None:
+            return self.core.box_muller(u1, u2)
+        return O.box_muller(u1, u2)
+
+    def burn_philox_gaussian(self, key, pos, n, mean=0.0, stddev=1.0, precision="fp32", out=None):
+        """One gaussian cycle like rngburn.gaussian_generate_kernel chunks
+        (rngburn.py:78-91): each even-aligned chunk draws its words, the core's
+        box_muller (_core.pyx:105-122) on (1 - u1, u2), x stddev + mean in
+        fp64, cast (distributions.py:116-131)."""
+        dtype = np.float32 if precision == "fp32" else np.float64
+        if out is None:
+            out = np.empty(n, dtype=dtype)
+        chunk = max(4096, -(-n // (4 * self.workers)))
+        chunk += chunk & 1
+
+        def gen(start):
+            stop = min(n, start + chunk)
+            m = stop - start
+            w = self._philox_fill(key, pos + start, m + (m & 1))
+            u1 = (w[0::2] >> np.uint32(8)).astype(np.float64) * O.UNIT_SCALE
+            u2 = (w[1::2] >> np.uint32(8)).astype(np.float64) * O.UNIT_SCALE
+            z0, z1 = self._box_muller(1.0 - u1, u2)
+            z = np.empty(2 * len(u1), dtype=np.float64)
+            z[0::2] = z0
+            z[1::2] = z1
+            z *= stddev
+            z += mean
+            out[start:stop] = z[:m]
+
+        list(self.pool.map(gen, range(0, n, chunk)))
+        return out
+
+    def time_cycle(self, fn, reps=3):
+        """Best-of-reps seconds of fn()."""
+        best = float("inf")
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            best = min(best, time.perf_counter() - t0)
+        return best
+
     def time_philox_uniform(self, n, reps=3, key=(777, 0), pos=0):
         """Best-of-reps seconds for one cycle of n fp32 uniforms (plus the output)."""
         out = np.empty(n, dtype=np.float32)

@@ -124,3 +124,25 @@ def test_restatement_matches_reference_core():
     c0, c1 = core.box_muller(u1, u2)
     o0, o1 = O.box_muller(u1, u2)
     assert np.array_equal(c0, o0) and np.array_equal(c1, o1)
+
+
+def test_cpu_baseline_cycles_match_oracle():
+    """bench.py's cpu_baseline legs (reference core, chunked threads) produce
+    the oracle's stream: uniform fp32, MRG fp64 [-1, 1), gaussian fp32 with an
+    odd count and an odd start position (pairs relative to the start)."""
+    from oracle.cpu_baseline import CpuPath
+
+    c = CpuPath(workers=3)
+    try:
+        key = O.seed_philox(777)
+        n = 3 * 4096 + 5
+        u = c.burn_philox_uniform(key, 7, n)
+        assert np.array_equal(u, O.words_to_unit(O.philox_words(key, 7, n), "fp32"))
+        s1, s2 = O.seed_mrg(777)
+        m = c.burn_mrg_uniform(s1, s2, 5001, -1.0, 1.0, "fp64")
+        assert np.array_equal(m, O.range_transform(O.words_to_unit(O.mrg_fill(*s1, *s2, 5001)[0], "fp64"), -1.0, 1.0))
+        g = c.burn_philox_gaussian(key, 3, n)
+        words = O.philox_words(key, 3, n + 1)
+        assert np.array_equal(g, O.gaussian_from_words(words, 0.0, 1.0, n, "fp32"))
+    finally:
+        c.close()
