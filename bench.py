@@ -467,10 +467,19 @@ def run_ours(args):
     from paper_2109_01329_b200.sharding import shard_state, weak_shard
 
     rank, world, local = dist_env()
+    # PRNG_BENCH_SHARE_GPU=1: dry run of the multi-rank path with several
+    # ranks on the same GPU(s) (gloo: NCCL refuses duplicate devices); timing
+    # from such a run is not a scaling number.
+    share = os.environ.get("PRNG_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=dev)
+        if share:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=dev)
 
     engine, dist, prec, n_default, desc = WORKLOADS[args.workload]
     n = args.n or n_default
@@ -491,7 +500,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            tdist.barrier(device_ids=[local])
+            if share:
+                tdist.barrier()
+            else:
+                tdist.barrier(device_ids=[local])
 
     for _ in range(args.warmup):
         P.generate(spec, st, n, out=out)
@@ -628,7 +640,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
-    ap.add_argument("--n", type=int, default=0, help="samples per GPU (default: the workload's)")
+    ap.add_argument("--n", "--n-per-gpu", dest="n", type=int, default=0,
+                    help="samples per GPU (default: the workload's; use --n-per-gpu under torchrun)")
     ap.add_argument("--e2e-n", type=int, default=1 << 30)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-n", type=int, default=1 << 27)
