@@ -775,6 +775,8 @@ int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double dis
     if (!rc) rc = check_method(method);
     if (rc) return rc;
     const XformParams p = logn_params(m, s, displ, scale);
+    if (method == PRNG_METHOD_FAST && p.ln_scale_f == 1.0f && p.ln_displ_f == 0.0f)  // oneMKL's default form
+        return launch_philox<kLognF32FastUnit>(k0, k1, ctr, lane, n, out, p, stream);
     return method == PRNG_METHOD_FAST ? launch_philox<kLognF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
                                       : launch_philox<kLognF32Accurate>(k0, k1, ctr, lane, n, out, p, stream);
 }

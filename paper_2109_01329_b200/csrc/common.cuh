@@ -248,7 +248,10 @@ enum Xform : int {
     kUnitF64 = 10,
     kGaussF32Exact = 11,  // the reference's fp64 Box-Muller bit for bit, cast once
     kGaussF64Exact = 12,
+    kLognF32FastUnit = 13,  // kLognF32Fast with scale 1, displ 0 (no final affine: bit-identical)
 };
+
+constexpr bool is_logn_fast(int X) { return X == kLognF32Fast || X == kLognF32FastUnit; }
 
 template <int X> struct XformTraits;
 template <> struct XformTraits<kBits> { using T = uint32_t; static constexpr bool kPair = false; };
@@ -260,6 +263,7 @@ template <> struct XformTraits<kGaussF32Fast> { using T = float; static constexp
 template <> struct XformTraits<kGaussF32Accurate> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kGaussF64> { using T = double; static constexpr bool kPair = true; };
 template <> struct XformTraits<kLognF32Fast> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kLognF32FastUnit> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kLognF32Accurate> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kLognF64> { using T = double; static constexpr bool kPair = true; };
 template <> struct XformTraits<kGaussF32Exact> { using T = float; static constexpr bool kPair = true; };
@@ -459,17 +463,17 @@ __device__ __forceinline__ float2* sincos_tab() {
 // also folds log2(e), removing the exp's argument multiplies.
 template <int X>
 constexpr bool bm_table_scaled() {
-    return X == kGaussF32Fast || X == kLognF32Fast;
+    return X == kGaussF32Fast || is_logn_fast(X);
 }
 constexpr float kLog2E = 1.4426950408889634f;
 
 template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform_prologue(const XformParams& p) {
-    if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
+    if constexpr (X == kGaussF32Fast || is_logn_fast(X)) {
         float2* tab = sincos_tab<TL>();
         // lognormal: also log2(e), so exp(m + s z) = ex2(fma(rq, cs', m log2(e)))
         const float S = !bm_table_scaled<X>() ? 1.0f
-                        : X == kLognF32Fast   ? p.scale_f * kBmRq * kLog2E
+                        : is_logn_fast(X)     ? p.scale_f * kBmRq * kLog2E
                                               : p.scale_f * kBmRq;
         for (int i = threadIdx.x; i < (1 << TL); i += blockDim.x) {
             float sn, cs;
@@ -624,7 +628,7 @@ template <> __device__ __forceinline__ void xform2<kLognF32Accurate>(uint32_t w0
 template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformParams& p,
                                         typename XformTraits<X>::T& o0, typename XformTraits<X>::T& o1) {
-    if constexpr (X == kGaussF32Fast || X == kLognF32Fast) {
+    if constexpr (X == kGaussF32Fast || is_logn_fast(X)) {
         float rq, sn, cs;
         box_muller_f32_parts<TL>(w0, w1, rq, sn, cs);
         // stddev and sqrt(2 ln 2) folded into r (loop-invariant) or into the table
@@ -639,8 +643,13 @@ __device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformPar
             float e0, e1;
             asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(fmaf(rs, cs, off2)));
             asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(fmaf(rs, sn, off2)));
-            o0 = fmaf(e0, p.ln_scale_f, p.ln_displ_f);
-            o1 = fmaf(e1, p.ln_scale_f, p.ln_displ_f);
+            if constexpr (X == kLognF32FastUnit) {  // fma(e, 1, 0) == e
+                o0 = e0;
+                o1 = e1;
+            } else {
+                o0 = fmaf(e0, p.ln_scale_f, p.ln_displ_f);
+                o1 = fmaf(e1, p.ln_scale_f, p.ln_displ_f);
+            }
         }
     } else {
         xform2<X>(w0, w1, p, o0, o1);

@@ -121,7 +121,7 @@ constexpr bool philox_rk() {
 // of pass i) for the fast fp32 Box-Muller transforms.
 template <int X>
 constexpr bool philox_pipelined() {
-    return PRNG_PHILOX_PIPE && (X == kGaussF32Fast || X == kLognF32Fast);
+    return PRNG_PHILOX_PIPE && (X == kGaussF32Fast || is_logn_fast(X));
 }
 template <> struct PhiloxBpt<double> { static constexpr int kValue = 2; };
 
