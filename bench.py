@@ -53,7 +53,7 @@ KERNEL_NAMES = {
     "c1": "philox_kernel<kUnitF32, SHIFT=0>",
     "c2": "mrg_kernel<kUniformF64>",
     "c3_gauss": "philox_kernel<kGaussF32Fast, SHIFT=0>",
-    "c3_logn": "philox_kernel<kLognF32Fast, SHIFT=0>",
+    "c3_logn": "philox_kernel<kLognF32FastUnit, SHIFT=0>",
 }
 
 
