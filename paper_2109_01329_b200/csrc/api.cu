@@ -482,7 +482,7 @@ int check_mrg_state(const uint32_t* s1, const uint32_t* s2) {
 struct MrgTables {
     uint32_t nbits;
     uint32_t j1[kMrgMaxBits][9], j2[kMrgMaxBits][9];  // A^(seg * 2^b)
-    uint32_t h1[9], h2[9];                              // A^(32*chunk/chains)
+    MrgJump hs1, hs2;                                   // A^(32*chunk/chains), split
     MrgJump b1, b2;                                     // A^(31*seg), split
 };
 std::mutex g_mrg_mu;
@@ -511,10 +511,8 @@ MrgTables mrg_tables(uint64_t chunk, uint64_t seg, uint32_t nbits, uint64_t chai
     t.nbits = nbits;
     Mat3 a, b;
     mat_pow_u64(32 * chunk / chains, &a, &b);
-    for (int e = 0; e < 9; ++e) {
-        t.h1[e] = (uint32_t)a.v[e];
-        t.h2[e] = (uint32_t)b.v[e];
-    }
+    t.hs1 = split_jump(a, kMrgM1);
+    t.hs2 = split_jump(b, kMrgM2);
     mat_pow_u64(31 * seg, &a, &b);
     t.b1 = split_jump(a, kMrgM1);
     t.b2 = split_jump(b, kMrgM2);
@@ -573,8 +571,8 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     a.nbits = nbits;
     memcpy(a.j1, tb.j1, sizeof a.j1);
     memcpy(a.j2, tb.j2, sizeof a.j2);
-    memcpy(a.h1, tb.h1, sizeof a.h1);
-    memcpy(a.h2, tb.h2, sizeof a.h2);
+    a.hs1 = tb.hs1;
+    a.hs2 = tb.hs2;
     a.b1 = tb.b1;
     a.b2 = tb.b2;
     a.out = dptr;

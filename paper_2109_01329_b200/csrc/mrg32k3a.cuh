@@ -72,11 +72,33 @@ struct MrgLaunch {
     uint32_t nbits;
     uint32_t j1[kMrgMaxBits][9];  // A^(seg * 2^b)
     uint32_t j2[kMrgMaxBits][9];
-    uint32_t h1[9], h2[9];  // A^(32*chunk/kChains): chain c -> chain c+1
+    MrgJump hs1, hs2;       // A^(32*chunk/kChains), split: chain c -> chain c+1
     MrgJump b1, b2;         // A^(31*seg): end of a segment -> start of the lane's next one
     void* out;
     XformParams p;
 };
+
+// y = B x mod m with B split as hi*2^16 + lo (tables in shared memory).
+__device__ __forceinline__ void mrg_jump_p(const double* hi, const double* lo, double m, double inv_m, double& x0,
+                                           double& x1, double& x2) {
+    double y[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double l = __fma_rn(lo[3 * i + 2], x2, __fma_rn(lo[3 * i + 1], x1, __dmul_rn(lo[3 * i], x0)));
+        const double h = __fma_rn(hi[3 * i + 2], x2, __fma_rn(hi[3 * i + 1], x1, __dmul_rn(hi[3 * i], x0)));
+        y[i] = mrg_reduce(__fma_rn(mrg_reduce(h, m, inv_m), 65536.0, l), m, inv_m);
+    }
+    x0 = y[0];
+    x1 = y[1];
+    x2 = y[2];
+}
+
+// split_jump (api.cu) on the device: entry v < m as symmetric residue = hi 2^16 + lo.
+__device__ __forceinline__ void split_entry(uint32_t v, uint32_t m, double& hi, double& lo) {
+    const double sv = mrg_sym(v, m);
+    hi = rint(sv * (1.0 / 65536.0));
+    lo = __fma_rn(-hi, 65536.0, sv);
+}
 
 __device__ __forceinline__ void mrg_jump(const MrgJump& B, double m, double inv_m, double& x0, double& x1,
                                          double& x2) {
@@ -177,11 +199,24 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
     constexpr int WARPS = kMrgThreads / 32;
     constexpr int NC = MrgPlan<X>::kChains;
     __shared__ uint4 stage[NC][WARPS][32 * 8];
-    __shared__ uint32_t sj1[kMrgMaxBits * 9], sj2[kMrgMaxBits * 9];
-
+    // Start-state tables J_b.  Segmented (plain fp64) kernels split them for
+    // the exact fp64 mat-vec (mrg_jump_p: ~2.5x less pipe time than the
+    // integer fold formulation, on the FP64 pipe that is idle during
+    // start-up; 9 KB of shared memory), the others (whose Box-Muller table
+    // leaves no room) keep the integer walk.
+    constexpr bool kF64Walk = MrgPlan<X>::kSegmented;
+    constexpr int kTabN = kF64Walk ? kMrgMaxBits * 9 : 1;
+    constexpr int kIntN = kF64Walk ? 1 : kMrgMaxBits * 9;
+    __shared__ double sjh1[kTabN], sjl1[kTabN], sjh2[kTabN], sjl2[kTabN];
+    __shared__ uint32_t sj1[kIntN], sj2[kIntN];
     for (uint32_t i = threadIdx.x; i < a.nbits * 9; i += blockDim.x) {
-        sj1[i] = a.j1[i / 9][i % 9];
-        sj2[i] = a.j2[i / 9][i % 9];
+        if constexpr (kF64Walk) {
+            split_entry(a.j1[i / 9][i % 9], kMrgM1, sjh1[i], sjl1[i]);
+            split_entry(a.j2[i / 9][i % 9], kMrgM2, sjh2[i], sjl2[i]);
+        } else {
+            sj1[i] = a.j1[i / 9][i % 9];
+            sj2[i] = a.j2[i / 9][i % 9];
+        }
     }
     xform_prologue<X, kMrgTabLog2>(a.p);
     __syncthreads();
@@ -193,22 +228,35 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
     if (w0 >= a.n) return;                  // whole warp idle (warp-uniform)
 
     const uint64_t q = w0 / a.seg + lane;  // lane's first segment, in units of seg
-    uint32_t x10 = a.s1[0], x11 = a.s1[1], x12 = a.s1[2], x20 = a.s2[0], x21 = a.s2[1], x22 = a.s2[2];
-    for (uint32_t b = 0; b < a.nbits; ++b) {
-        if ((q >> b) & 1) {
-            mat3_apply<kMrgC1>(&sj1[9 * b], x10, x11, x12);
-            mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
+    MrgStateF64 x;
+    if constexpr (kF64Walk) {
+        x = MrgStateF64{mrg_sym(a.s1[0], kMrgM1), mrg_sym(a.s1[1], kMrgM1), mrg_sym(a.s1[2], kMrgM1),
+                        mrg_sym(a.s2[0], kMrgM2), mrg_sym(a.s2[1], kMrgM2), mrg_sym(a.s2[2], kMrgM2)};
+        for (uint32_t b = 0; b < a.nbits; ++b) {
+            if ((q >> b) & 1) {
+                mrg_jump_p(&sjh1[9 * b], &sjl1[9 * b], (double)kMrgM1, 1.0 / (double)kMrgM1, x.x10, x.x11, x.x12);
+                mrg_jump_p(&sjh2[9 * b], &sjl2[9 * b], (double)kMrgM2, 1.0 / (double)kMrgM2, x.x20, x.x21, x.x22);
+            }
         }
+    } else {
+        uint32_t x10 = a.s1[0], x11 = a.s1[1], x12 = a.s1[2], x20 = a.s2[0], x21 = a.s2[1], x22 = a.s2[2];
+        for (uint32_t b = 0; b < a.nbits; ++b) {
+            if ((q >> b) & 1) {
+                mat3_apply<kMrgC1>(&sj1[9 * b], x10, x11, x12);
+                mat3_apply<kMrgC2>(&sj2[9 * b], x20, x21, x22);
+            }
+        }
+        x = MrgStateF64{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
+                        mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
     }
     MrgStateF64 st[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         if (c) {  // chain c starts one chain region (A^(32 chunk / NC)) after chain c-1
-            mat3_apply<kMrgC1>(a.h1, x10, x11, x12);
-            mat3_apply<kMrgC2>(a.h2, x20, x21, x22);
+            mrg_jump(a.hs1, (double)kMrgM1, 1.0 / (double)kMrgM1, x.x10, x.x11, x.x12);
+            mrg_jump(a.hs2, (double)kMrgM2, 1.0 / (double)kMrgM2, x.x20, x.x21, x.x22);
         }
-        st[c] = MrgStateF64{mrg_sym(x10, kMrgM1), mrg_sym(x11, kMrgM1), mrg_sym(x12, kMrgM1),
-                            mrg_sym(x20, kMrgM2), mrg_sym(x21, kMrgM2), mrg_sym(x22, kMrgM2)};
+        st[c] = x;
     }
 
     const uint64_t region = 32 * a.chunk / NC;  // words per chain region
