@@ -199,12 +199,12 @@ __global__ void __launch_bounds__(kMrgThreads, MrgPlan<X>::kMinBlocks) mrg_kerne
     constexpr int WARPS = kMrgThreads / 32;
     constexpr int NC = MrgPlan<X>::kChains;
     __shared__ uint4 stage[NC][WARPS][32 * 8];
-    // Start-state tables J_b.  Segmented (plain fp64) kernels split them for
+    // Start-state tables J_b.  The non-Box-Muller kernels split them for
     // the exact fp64 mat-vec (mrg_jump_p: ~2.5x less pipe time than the
     // integer fold formulation, on the FP64 pipe that is idle during
     // start-up; 9 KB of shared memory), the others (whose Box-Muller table
     // leaves no room) keep the integer walk.
-    constexpr bool kF64Walk = MrgPlan<X>::kSegmented;
+    constexpr bool kF64Walk = !XformTraits<X>::kPair;
     constexpr int kTabN = kF64Walk ? kMrgMaxBits * 9 : 1;
     constexpr int kIntN = kF64Walk ? 1 : kMrgMaxBits * 9;
     __shared__ double sjh1[kTabN], sjl1[kTabN], sjh2[kTabN], sjl2[kTabN];
