@@ -16,6 +16,12 @@ buffer.  `value` = all ranks' samples / max-over-ranks device time.
 (the paper's TTS shape: generate + transform + copy back), D2H bytes = the
 samples; no inputs are uploaded (the engine state is passed by value).
 
+`--gpus N` without a torchrun environment re-launches this script under
+`torch.distributed.run` with N ranks (one process per GPU, NCCL); under
+torchrun WORLD_SIZE must equal --gpus.  Before timing, every rank checks
+its first and last 4096 samples against the CPU oracle at its global
+offset r*n (the single-stream slice rule, rngburn.py:70-73).
+
 `--impl reference`: the reference's own CPU path (oracle/cpu_baseline.py:
 the compiled portarng kernel core from oracle/_ref driven the way
 burn_once(..., Parallel(ncpu)) drives it) on this host's cores, rank 0 only.
@@ -66,6 +72,78 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def relaunch(nproc):
+    """`bench.py --gpus N` outside torchrun: one process per GPU through
+    torch.distributed.run (the driver's own launch line), rank 0 prints."""
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    log("relaunch: " + " ".join(cmd))
+    return subprocess.call(cmd, env=env)
+
+
+def slice_windows(n, w=4096):
+    return [(0, min(w, n))] + ([(n - w, n)] if n > w else [])
+
+
+def slice_check(P, torch, workload, spec, out, n, rank):
+    """This rank's output equals the single-stream CPU oracle at global
+    element offset rank*n (first and last 4096 samples): the sharding rule
+    of rngburn.py:70-73 / execution.py:309-315.  Oracle = checker only,
+    outside the timed region."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from tests import tolerances as TOL
+
+    engine, dist, prec, _, _ = WORKLOADS[workload]
+    ok, worst = True, 0.0
+    for lo, hi in slice_windows(n):
+        g = rank * n + lo  # global element index
+        if engine == "philox":
+            st = ("philox", (O.seed_philox(777), g))  # words_consumed(g) == g (g even for pairs)
+        else:
+            st = ("mrg", O.mrg_skip(*O.seed_mrg(777), g))
+        a, b = (-1.0, 1.0) if (dist == "uniform" and prec == "fp64") else (0.0, 1.0)
+        want = O.generate(engine, st, dist, hi - lo, prec, a, b)
+        got = out[lo:hi].cpu().numpy()
+        if dist in ("bits", "uniform"):
+            ok &= bool(np.array_equal(got, want))
+        else:
+            dt = np.float32 if prec == "fp32" else np.float64
+            fast = getattr(spec, "method", "fast") == "fast"
+            allowed = (TOL.gaussian_allowed(want, 0.0, 1.0, dt, fast) if dist == "gaussian"
+                       else TOL.lognormal_allowed(want, 0.0, 1.0, dt, fast))
+            err = np.abs(got.astype(np.float64) - want.astype(np.float64))
+            ok &= bool(np.all(err <= allowed))
+            worst = max(worst, float(np.max(err / allowed)))
+    return ok, worst
+
+
+def device_info(torch, dev):
+    pr = torch.cuda.get_device_properties(dev)
+    return {"device": dev.index, "name": pr.name, "uuid": str(getattr(pr, "uuid", "")),
+            "pci_bus_id": getattr(pr, "pci_bus_id", None)}
+
+
+def host_mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
 
 
 def make_spec(P, dist, prec):
@@ -171,6 +249,35 @@ def metric_for(workload):
 
 
 def cpu_baseline_sample(n_cpu, workload="c4"):
+    """The reference's CPU path for the workload on a bounded sample: stock
+    rngburn.burn_once(engine, spec, "buffer", Parallel(os.cpu_count()), n,
+    777) from the staged reference (MRG32k3a runs one chunk: unsplittable in
+    the reference, rngburn.py:123); the restated core driver
+    (oracle/cpu_baseline.py) only if the reference is not staged."""
+    mods = import_stock_reference()
+    engine_kind, dist, prec, _, _ = WORKLOADS[workload]
+    if engine_kind == "mrg":
+        n_cpu = min(n_cpu, 1 << 24)
+    elif dist == "gaussian":
+        n_cpu = min(n_cpu, 1 << 25)
+    ncpu = os.cpu_count() or 1
+    if mods is not None:
+        engine, distributions, execution, rngburn, _K = mods
+        os.environ.setdefault(execution.ARENA_ENV_VAR, str(max(2 * 1024 ** 3, 8 * n_cpu)))
+        eng = engine.EngineKind.MRG32K3A if engine_kind == "mrg" else engine.EngineKind.PHILOX4X32X10
+        spec = (distributions.Gaussian(0.0, 1.0, prec) if dist == "gaussian"
+                else distributions.Uniform(-1.0, 1.0, prec) if prec == "fp64" else distributions.Uniform(0.0, 1.0, prec))
+        backend = execution.Parallel(workers=ncpu)
+        best = min(rngburn.burn_once(eng, spec, "buffer", backend, n_cpu, 777)[0] for _ in range(3)) / 1e9
+        return {"value": n_cpu / best / 1e9, "unit": "Gsamples/s", "cores": 1 if engine_kind == "mrg" else ncpu,
+                "kind": "reference", "host_cpu": cpu_model(),
+                "sample": f"stock rngburn.burn_once({eng.name}, {spec}, 'buffer', Parallel({ncpu}), n={n_cpu}, 777), "
+                          "compiled core, best of 3 TTS cycles"
+                          + (" (MRG32k3a unsplittable: one chunk, rngburn.py:123)" if engine_kind == "mrg" else "")}
+    return cpu_baseline_sample_restated(n_cpu, workload)
+
+
+def cpu_baseline_sample_restated(n_cpu, workload="c4"):
     """The reference's CPU path for the workload, on a bounded sample (the
     oracle/_ref core; MRG32k3a single-threaded: unsplittable in the
     reference, rngburn.py:123)."""
@@ -205,37 +312,129 @@ def cpu_baseline_sample(n_cpu, workload="c4"):
             "sample": f"{what}, best of 3, burn_once-style chunked threads={c.workers}"}
 
 
+STAGED_REF = ROOT / "baseline" / "_ref" / "pkg"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
+def import_stock_reference():
+    """The unmodified reference package (staged by baseline/stage_ref.sh) with
+    its compiled Cython core selected (PORTARNG_KERNELS=core)."""
+    if not (STAGED_REF / "src" / "portarng").is_dir():
+        return None
+    os.environ["PORTARNG_KERNELS"] = "core"
+    sys.path.insert(0, str(STAGED_REF / "src"))
+    import portarng._kernels as K
+    from portarng import distributions, engine, execution, rngburn
+
+    assert K.IMPL == "core", K.IMPL
+    return engine, distributions, execution, rngburn, K
+
+
+def kernel_bench_rates(K, repeat=3):
+    """benchmarks/kernel_bench.py:22-57 style: best-of single-thread rates of
+    the compiled core's three kernels (10^7 words / pairs, MRG 10^6)."""
+    import numpy as np
+
+    def best(fn):
+        ts = []
+        for _ in range(repeat):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    n, nm = 10 ** 7, 10 ** 6
+    rng = np.random.default_rng(1)
+    u1 = 1.0 - rng.integers(0, 2 ** 24, n // 2).astype(np.float64) / 2 ** 24
+    u2 = rng.integers(0, 2 ** 24, n // 2).astype(np.float64) / 2 ** 24
+    return {
+        "philox_fill_mwords_s": n / best(lambda: K.philox_fill(0xCAFE, 0xF00D, 0, 0, 0, 0, 0, n)) / 1e6,
+        "mrg_fill_mwords_s": nm / best(lambda: K.mrg_fill(12345, 12345, 12345, 12345, 12345, 12345, nm)) / 1e6,
+        "box_muller_mpairs_s": (n // 2) / best(lambda: K.box_muller(u1, u2)) / 1e6,
+        "threads": 1, "source": "reference benchmarks/kernel_bench.py kernels, best of %d" % repeat,
+    }
+
+
 def run_reference(args):
+    """The reference's own CPU path on this host: stock
+    rngburn.burn_once(PHILOX4X32X10, Uniform(0, 1, fp32), "buffer",
+    Parallel(os.cpu_count()), n, 777) (rngburn.py:111-151) from the staged,
+    unmodified reference with its compiled core; rank 0 only.  Each step is
+    one full TTS cycle (seed, device-arena allocation, chunked generate,
+    affine pass, host copy) on a bounded n (--ref-n, default 2^28)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from oracle.cpu_baseline import CpuPath
-
-    engine, dist, prec, n_default, desc = WORKLOADS["c4"]
     n = args.ref_n
-    c = CpuPath()
-    import numpy as np
+    ncpu = os.cpu_count() or 1
+    mods = import_stock_reference()
+    extra = {}
+    if mods is not None:
+        engine, distributions, execution, rngburn, K = mods
+        os.environ.setdefault(execution.ARENA_ENV_VAR, str(max(2 * 1024 ** 3, 8 * n)))
+        eng = engine.EngineKind.PHILOX4X32X10
+        spec = distributions.Uniform(0.0, 1.0, "fp32")
+        backend = execution.Parallel(workers=ncpu)
 
-    out = np.empty(n, dtype=np.float32)
-    for i in range(args.warmup):
-        c.burn_philox_uniform((777, 0), i * n, n, out=out)
+        def step():
+            tts, host = rngburn.burn_once(eng, spec, "buffer", backend, n, 777)
+            return tts / 1e9, host
+
+        kind = "reference"
+        what = (f"stock portarng rngburn.burn_once(PHILOX4X32X10, Uniform(0,1,fp32), 'buffer', "
+                f"Parallel({ncpu}), n={n}, seed=777), compiled Cython core (PORTARNG_KERNELS=core)")
+    else:  # pragma: no cover - reference not staged: the restated core driver
+        from oracle.cpu_baseline import CpuPath
+
+        import numpy as np
+
+        c = CpuPath()
+        out = np.empty(n, dtype=np.float32)
+
+        def step():
+            t0 = time.perf_counter()
+            c.burn_philox_uniform((777, 0), 0, n, out=out)
+            return time.perf_counter() - t0, out
+
+        kind, what = c.kind, f"oracle/cpu_baseline.py CpuPath (reference core), n={n}, {c.workers} threads"
+    for _ in range(args.warmup):
+        _, host = step()
     times = []
-    for i in range(args.steps):
-        t0 = time.perf_counter()
-        c.burn_philox_uniform((777, 0), (args.warmup + i) * n, n, out=out)
-        times.append(time.perf_counter() - t0)
-    c.close()
+    for _ in range(args.steps):
+        t, host = step()
+        times.append(t)
+    # the cycle's output is the reference's stream (SURVEY Appendix A: first4)
+    assert abs(float(host[0]) - 0.35297131538391113) < 1e-12 and len(host) == n
     total = sum(times)
     value = n * args.steps / total / 1e9
+    if mods is not None and not args.no_secondary:
+        hd = []
+        for _ in range(2):
+            tts, _h = rngburn.burn_once(eng, spec, "hostdirect", execution.Serial(), n, 777)
+            hd.append(tts / 1e9)
+        extra["hostdirect_serial_gsamples_s"] = n / min(hd) / 1e9
+        extra["kernel_bench_single_thread"] = kernel_bench_rates(K)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Gsamples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32->f32",
         "data": "synthetic (counter-based RNG: no input data)",
-        "config": {"workload": desc + f"; CPU bounded sample n={n} per step", "n_per_step": n,
-                   "l2": "n/a (CPU)"},
-        "cpu_baseline": {"value": value, "unit": "Gsamples/s", "cores": c.workers, "kind": c.kind,
-                         "sample": f"n={n} fp32 uniforms per step, chunked over {c.workers} threads"},
+        "config": {"workload": WORKLOADS["c4"][4] + f"; CPU bounded sample n={n} per step", "n_per_step": n,
+                   "l2": "n/a (CPU)", "host_cpu": cpu_model(), "os_cpu_count": ncpu,
+                   "timing": "rngburn's own perf_counter_ns TTS per cycle (rngburn.py:124-150)"},
+        "cpu_baseline": {"value": value, "unit": "Gsamples/s", "cores": ncpu, "kind": kind, "sample": what},
+        "secondary": extra or None,
         "e2e": {"value": value, "unit": "Gsamples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -467,19 +666,35 @@ def run_ours(args):
     from paper_2109_01329_b200.sharding import shard_state, weak_shard
 
     rank, world, local = dist_env()
-    # PRNG_BENCH_SHARE_GPU=1: dry run of the multi-rank path with several
-    # ranks on the same GPU(s) (gloo: NCCL refuses duplicate devices); timing
-    # from such a run is not a scaling number.
-    share = os.environ.get("PRNG_BENCH_SHARE_GPU") == "1"
+    if args.gpus is not None and args.gpus != world:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
+    # PRNG_BENCH_SHARE_GPU=1 (or fewer visible GPUs than ranks): functional
+    # dry run of the multi-rank path with several ranks on the same GPU(s)
+    # (gloo: NCCL refuses duplicate devices); timing from such a run is not a
+    # scaling number and the line says so.
+    ndev = torch.cuda.device_count()
+    share = os.environ.get("PRNG_BENCH_SHARE_GPU") == "1" or world > ndev
     if share:
-        local = local % torch.cuda.device_count()
+        if world > 1:
+            log(f"bench: {world} ranks on {ndev} visible GPU(s): shared-GPU dry run (gloo), not a scaling number")
+        local = local % ndev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    ranks_info = [device_info(torch, dev)]
+    backend = None
     if world > 1:
+        backend = "gloo" if share else "nccl"
         if share:
             tdist.init_process_group("gloo")
         else:
             tdist.init_process_group("nccl", device_id=dev)
+            one = torch.ones(1, device=dev)
+            tdist.all_reduce(one)  # forces NCCL communicator init (NCCL_DEBUG=INFO logs it)
+            assert int(one.item()) == world, "NCCL all_reduce did not see every rank"
+        gathered = [None] * world
+        tdist.all_gather_object(gathered, dict(ranks_info[0], rank=rank))
+        ranks_info = gathered
+        assert tdist.get_world_size() == world
 
     engine, dist, prec, n_default, desc = WORKLOADS[args.workload]
     n = args.n or n_default
@@ -508,6 +723,20 @@ def run_ours(args):
     for _ in range(args.warmup):
         P.generate(spec, st, n, out=out)
     torch.cuda.synchronize()
+    check = None
+    if not args.no_check:
+        ok, worst = slice_check(P, torch, args.workload, spec, out, n, rank)
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        if world > 1:
+            tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+        check = {"ranks": world, "windows_per_rank": len(slice_windows(n)), "samples_per_window": 4096,
+                 "all_equal": bool(flag.item()),
+                 "rule": "rank r's samples == CPU oracle at global offset r*n (first and last 4096)",
+                 "mode": "bit-exact" if dist in ("bits", "uniform") else "stated tolerance (tests/tolerances.py)"}
+        if dist not in ("bits", "uniform"):
+            check["worst_err_over_allowed_rank0"] = worst
+        if not check["all_equal"]:
+            raise SystemExit(f"bench: slice check failed on some rank: {check}")
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -542,10 +771,49 @@ def run_ours(args):
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     traffic = ncu_traffic(args.workload, n)
 
+    # ---- sustained series (outside the timed region): the board power cap
+    # engages ~60 ms into back-to-back launches, so a short K reads burst ----
+    sustained = None
+    if args.sustained and flush is None:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with ClockSampler(local) as clk2:
+            ev[0].record(stream)
+            for _ in range(args.sustained):
+                P.generate(spec, st, n, out=out)
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+        sms = ev[0].elapsed_time(ev[1]) / args.sustained
+        sustained = {"launches": args.sustained, "ms_per_launch": sms, "gsamples_s_per_gpu": n / sms / 1e6,
+                     "achieved_gbs": n * esize / sms / 1e6, "clocks": clk2.summary()}
+
+    # ---- write ceiling: in-repo write-only probe, same grid and store pattern ----
+    write_peak = None
+    if esize == 4 and n * esize % 64 == 0 and not args.no_probe:
+        lib = P._lib.lib
+        h = stream.cuda_stream
+        for _ in range(3):
+            P._lib.check(lib.prng_diag_write_probe(out.data_ptr(), n * esize, h))
+        pe = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        reps = 10
+        pe[0].record(stream)
+        for _ in range(reps):
+            P._lib.check(lib.prng_diag_write_probe(out.data_ptr(), n * esize, h))
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        pms = pe[0].elapsed_time(pe[1]) / reps
+        write_peak = {"achieved_gbs": n * esize / pms / 1e6, "ms_per_launch": pms, "reps": reps,
+                      "source": "prng_diag_write_probe: 256-bit streaming stores, same grid as the kernel, "
+                                "no generator work (burst, back to back)"}
+
     # ---- end to end: public API into pinned host memory ----
     e2e = None
     if not args.no_e2e:
-        n_e2e = min(n, args.e2e_n)
+        # same size as `value` when the host can pin it for every rank
+        # (<= 1/4 of MemAvailable), else the largest power of two that fits
+        n_e2e = n if args.e2e_n is None else min(n, args.e2e_n)
+        avail = host_mem_available()
+        while avail and n_e2e > (1 << 20) and world * n_e2e * esize > avail // 4:
+            n_e2e //= 2
         host = torch.empty(n_e2e, dtype=dtype, pin_memory=True)
         best = None
         for strategy in ("zero_copy", "pipelined"):
@@ -604,6 +872,7 @@ def run_ours(args):
                 "global_samples_per_step": n * world,
                 "sharding": "rank r owns stream words [r*n, (r+1)*n) (skip_ahead offsets, no collective)",
                 "parallelism": f"replica-free counter sharding x{world}",
+                "shared_gpu_dry_run": bool(share and world > 1),
                 "l2": ("output buffer %.1f GiB > 126 MB L2 (no flush needed)" % (n * esize / 2**30))
                 if flush is None else "512 MiB L2 flush (write, then a 512 MiB read sweep) between steps, outside the per-launch timing",
             },
@@ -618,7 +887,16 @@ def run_ours(args):
                 "algorithmic_bytes_per_launch": alg_bytes,
                 "peak_source": peak_src,
                 "kernel_ms": kern_ms,
+                "write_peak": write_peak,
+                "frac_of_write_peak": achieved / write_peak["achieved_gbs"] if write_peak else None,
+                "sustained": sustained,
+                "sustained_frac": sustained["achieved_gbs"] / peak if sustained else None,
+                "sustained_frac_of_write_peak": (sustained["achieved_gbs"] / write_peak["achieved_gbs"]
+                                                 if sustained and write_peak else None),
             },
+            "slice_check": check,
+            "ranks": ranks_info,
+            "backend": backend,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps,
@@ -635,23 +913,31 @@ def run_ours(args):
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (one per GPU); without torchrun, >1 re-launches under torch.distributed.run")
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--n", "--n-per-gpu", dest="n", type=int, default=0,
                     help="samples per GPU (default: the workload's; use --n-per-gpu under torchrun)")
-    ap.add_argument("--e2e-n", type=int, default=1 << 30)
+    ap.add_argument("--e2e-n", type=int, default=None, help="e2e samples per GPU (default: the value's n)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-n", type=int, default=1 << 27)
-    ap.add_argument("--ref-n", type=int, default=1 << 26)
+    ap.add_argument("--ref-n", type=int, default=1 << 28, help="reference arm: samples per TTS cycle")
+    ap.add_argument("--no-secondary", action="store_true", help="reference arm: skip hostdirect + kernel rates")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the per-rank oracle slice check")
+    ap.add_argument("--no-probe", action="store_true", help="skip the write-ceiling probe")
+    ap.add_argument("--sustained", type=int, default=150,
+                    help="back-to-back launches after the timed region for the sustained number (0 = off)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sweep", action="store_true", help="also run the C4 batch-size sweep (CUDA-graph timed)")
     ap.add_argument("--sweep-max", type=int, default=32)
     ap.add_argument("--events", type=int, default=10000, help="C5 event count")
     args = ap.parse_args()
+    if args.gpus is not None and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     if args.warmup < 3:
         log("warning: contract requires --warmup >= 3")
     if args.impl == "reference":

@@ -9,7 +9,10 @@
  * Conventions
  *  - Plain pointers and sizes only; no allocation on the device entry points,
  *    no host synchronisation, stream-ordered on `stream` (a cudaStream_t;
- *    NULL = legacy default stream).  The device is taken from `out`.
+ *    NULL = legacy default stream).  The device is taken from `out` for the
+ *    duration of the call; the caller's current device is restored on
+ *    return.  (One exception: the first PRNG_METHOD_EXACT request on a
+ *    device builds its correction tables -- see below.)
  *  - `out` is caller-owned device memory (or mapped pinned host memory),
  *    aligned to its element size.
  *  - Philox state arguments are exactly those of the reference kernel
@@ -57,8 +60,10 @@ extern "C" {
  * approximations of log(u1') and (sin t, cos t) are corrected to the host
  * libm's values by 4-bit ulp deltas tabulated over their whole 2^24-point
  * domains (~24 MB per device plus short escape lists, built once per
- * process; prng_exact_tables_prepare builds them ahead of the first
- * request). */
+ * device; prng_exact_tables_prepare builds them ahead of the first
+ * request).  The build runs on a private stream in relaxed capture mode, so
+ * a first exact request inside CUDA-graph capture works; it blocks the
+ * calling thread for about a second. */
 #define PRNG_METHOD_EXACT 2
 
 int prng_abi_version(void);
@@ -195,6 +200,13 @@ int prng_kernels_philox_fill(uint32_t k0, uint32_t k1, uint32_t b0, uint32_t b1,
 int prng_kernels_mrg_fill(uint32_t s10, uint32_t s11, uint32_t s12, uint32_t s20, uint32_t s21, uint32_t s22,
                           uint64_t n, uint32_t *host_out, uint32_t s1_out[3], uint32_t s2_out[3]);
 int prng_kernels_box_muller(const double *u1, const double *u2, uint64_t m, double *z0, double *z1);
+
+/* ---- Diagnostics. ----
+ * Write-only roofline probe: fills `bytes` (a multiple of 64) of 32-byte
+ * aligned device memory with the grid shape and 256-bit streaming-store
+ * pattern of the aligned Philox 4-byte kernel, and no generator arithmetic;
+ * bench.py times it next to the headline kernel as the HBM write ceiling. */
+int prng_diag_write_probe(void *out, uint64_t bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,7 @@ SIGNATURES = {
     "prng_kernels_philox_fill": ([_u32] * 7 + [_u64, _vp], _int),
     "prng_kernels_mrg_fill": ([_u32] * 6 + [_u64, _vp, _u32p, _u32p], _int),
     "prng_kernels_box_muller": ([_vp, _vp, _u64, _vp, _vp], _int),
+    "prng_diag_write_probe": ([_vp, _u64, _vp], _int),
 }
 
 

@@ -56,7 +56,26 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-// ---- device resolution: the device that owns `ptr` becomes current ----
+// ---- device resolution: the device that owns `ptr` becomes current for the
+// duration of the entry point; DeviceGuard (declared first in every extern "C"
+// entry that launches) switches the caller's device back on return, so a
+// generate into a tensor on cuda:3 never leaves cuda:3 current.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 int bind_output(const void* ptr, void** dev_ptr) {
     cudaPointerAttributes attr;
     cudaError_t e = cudaPointerGetAttributes(&attr, ptr);
@@ -84,6 +103,18 @@ struct DeviceInfo {
 };
 std::mutex g_mu;
 std::map<int, DeviceInfo> g_dev;
+
+// SM count of the current device (cached; 148 on B200, queried so that a
+// partitioned / MIG device or another part gets a grid sized for it).
+int device_sms(int* sms_out) {
+    int dev = 0;
+    PRNG_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceInfo& di = g_dev[dev];
+    if (di.sms == 0) PRNG_CUDA(cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, dev));
+    *sms_out = di.sms;
+    return PRNG_OK;
+}
 
 int resident_ctas(const void* kernel, int threads, int* sms_out, int* occ_out) {
     int dev = 0;
@@ -187,76 +218,111 @@ inline uint8_t nibble(double want, double approx) {
     return 8;
 }
 
+// Builds (once per device) and binds the correction tables.  Safe to call
+// while a stream of this thread is being captured into a CUDA graph: the
+// build switches this thread to relaxed capture mode and works on a private
+// non-blocking stream with stream-ordered allocations, so nothing touches
+// the legacy stream or synchronises the device.  The host libm tables
+// (384 MB) are released after the upload unless prng_exact_tables_host
+// asked for them.
+bool g_exact_keep_host = false;
+
+int exact_tables_build(ExactDevice& ed, cudaStream_t st) {
+    if (g_exact_log.empty()) build_exact_host_tables();
+    // 1. the device approximations over both whole domains
+    double* dL = nullptr;
+    PRNG_CUDA(cudaMallocAsync((void**)&dL, 3 * kExactN * sizeof(double), st));
+    double* dS = dL + kExactN;
+    double* dC = dS + kExactN;
+    exact_approx_kernel<<<1184, 256, 0, st>>>(dL, dS, dC);
+    std::vector<double> aL(kExactN), aS(kExactN), aC(kExactN);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(aL.data(), dL, kExactN * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(aS.data(), dS, kExactN * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(aC.data(), dC, kExactN * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(dL, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "exact tables: approximations");
+    // 2. ulp corrections to the host libm, escapes where they do not fit
+    std::vector<uint8_t> lnib(kExactN / 2), scnib(kExactN);
+    for (size_t i = 0; i < kExactN; i += 2)
+        lnib[i / 2] = (uint8_t)(nibble(g_exact_log[i], aL[i]) | (nibble(g_exact_log[i + 1], aL[i + 1]) << 4));
+    for (size_t i = 0; i < kExactN; ++i)
+        scnib[i] = (uint8_t)(nibble(g_exact_sc[i].x, aS[i]) | (nibble(g_exact_sc[i].y, aC[i]) << 4));
+    std::vector<uint32_t> eidx[3];
+    std::vector<double> eval[3];
+    for (size_t i = 0; i < kExactN; ++i) {
+        if (((lnib[i / 2] >> ((i & 1) * 4)) & 0xF) == 8) {
+            eidx[0].push_back((uint32_t)i);
+            eval[0].push_back(g_exact_log[i]);
+        }
+        if ((scnib[i] & 0xF) == 8) {
+            eidx[1].push_back((uint32_t)i);
+            eval[1].push_back(g_exact_sc[i].x);
+        }
+        if ((scnib[i] >> 4) == 8) {
+            eidx[2].push_back((uint32_t)i);
+            eval[2].push_back(g_exact_sc[i].y);
+        }
+    }
+    // 3. upload: one long-lived allocation (nibbles, then each escape list)
+    size_t bytes = lnib.size() + scnib.size();
+    for (int t = 0; t < 3; ++t) bytes += eidx[t].size() * 12 + 16;
+    char* base = nullptr;
+    PRNG_CUDA(cudaMalloc(&base, bytes));
+    char* q = base;
+    PRNG_CUDA(cudaMemcpyAsync(q, lnib.data(), lnib.size(), cudaMemcpyHostToDevice, st));
+    ed.corr.log_nib = reinterpret_cast<const uint8_t*>(q);
+    q += lnib.size();
+    PRNG_CUDA(cudaMemcpyAsync(q, scnib.data(), scnib.size(), cudaMemcpyHostToDevice, st));
+    ed.corr.sc_nib = reinterpret_cast<const uint8_t*>(q);
+    q += scnib.size();
+    for (int t = 0; t < 3; ++t) {
+        const size_t ne = eidx[t].size();
+        PRNG_CUDA(cudaMemcpyAsync(q, eval[t].data(), ne * 8, cudaMemcpyHostToDevice, st));
+        ed.corr.esc_val[t] = reinterpret_cast<const double*>(q);
+        q += ne * 8 + 8;
+        PRNG_CUDA(cudaMemcpyAsync(q, eidx[t].data(), ne * 4, cudaMemcpyHostToDevice, st));
+        ed.corr.esc_idx[t] = reinterpret_cast<const uint32_t*>(q);
+        q += (ne * 4 + 8) / 8 * 8;
+        ed.corr.esc_n[t] = (uint32_t)ne;
+        ed.escapes += ne;
+    }
+    PRNG_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+    return PRNG_OK;
+}
+
 int exact_tables(XformParams& p) {
     int dev = 0;
     PRNG_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(g_exact_mu);
     auto it = g_exact_corr.find(dev);
     if (it == g_exact_corr.end()) {
-        if (g_exact_log.empty()) build_exact_host_tables();
-        // 1. the device approximations over both whole domains
-        double *dL = nullptr, *dS = nullptr, *dC = nullptr;
-        PRNG_CUDA(cudaMalloc(&dL, 3 * kExactN * sizeof(double)));
-        dS = dL + kExactN;
-        dC = dS + kExactN;
-        exact_approx_kernel<<<1184, 256>>>(dL, dS, dC);
-        std::vector<double> aL(kExactN), aS(kExactN), aC(kExactN);
-        cudaError_t e = cudaMemcpy(aL.data(), dL, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
-        if (e == cudaSuccess) e = cudaMemcpy(aS.data(), dS, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
-        if (e == cudaSuccess) e = cudaMemcpy(aC.data(), dC, kExactN * sizeof(double), cudaMemcpyDeviceToHost);
-        cudaFree(dL);
-        if (e != cudaSuccess) return cuda_fail(e, "exact tables: approximations");
-        // 2. ulp corrections to the host libm, escapes where they do not fit
-        std::vector<uint8_t> lnib(kExactN / 2), scnib(kExactN);
-        for (size_t i = 0; i < kExactN; i += 2)
-            lnib[i / 2] = (uint8_t)(nibble(g_exact_log[i], aL[i]) | (nibble(g_exact_log[i + 1], aL[i + 1]) << 4));
-        for (size_t i = 0; i < kExactN; ++i)
-            scnib[i] = (uint8_t)(nibble(g_exact_sc[i].x, aS[i]) | (nibble(g_exact_sc[i].y, aC[i]) << 4));
-        std::vector<uint32_t> eidx[3];
-        std::vector<double> eval[3];
-        for (size_t i = 0; i < kExactN; ++i) {
-            if (((lnib[i / 2] >> ((i & 1) * 4)) & 0xF) == 8) {
-                eidx[0].push_back((uint32_t)i);
-                eval[0].push_back(g_exact_log[i]);
-            }
-            if ((scnib[i] & 0xF) == 8) {
-                eidx[1].push_back((uint32_t)i);
-                eval[1].push_back(g_exact_sc[i].x);
-            }
-            if ((scnib[i] >> 4) == 8) {
-                eidx[2].push_back((uint32_t)i);
-                eval[2].push_back(g_exact_sc[i].y);
-            }
-        }
-        // 3. upload: one allocation (nibbles, then each escape list)
-        size_t bytes = lnib.size() + scnib.size();
-        for (int t = 0; t < 3; ++t) bytes += eidx[t].size() * 12 + 16;
-        char* base = nullptr;
-        PRNG_CUDA(cudaMalloc(&base, bytes));
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        PRNG_CUDA(cudaThreadExchangeStreamCaptureMode(&mode));
+        cudaStream_t st = nullptr;
         ExactDevice ed;
-        char* q = base;
-        PRNG_CUDA(cudaMemcpy(q, lnib.data(), lnib.size(), cudaMemcpyHostToDevice));
-        ed.corr.log_nib = reinterpret_cast<const uint8_t*>(q);
-        q += lnib.size();
-        PRNG_CUDA(cudaMemcpy(q, scnib.data(), scnib.size(), cudaMemcpyHostToDevice));
-        ed.corr.sc_nib = reinterpret_cast<const uint8_t*>(q);
-        q += scnib.size();
-        for (int t = 0; t < 3; ++t) {
-            const size_t ne = eidx[t].size();
-            PRNG_CUDA(cudaMemcpy(q, eval[t].data(), ne * 8, cudaMemcpyHostToDevice));
-            ed.corr.esc_val[t] = reinterpret_cast<const double*>(q);
-            q += ne * 8 + 8;
-            PRNG_CUDA(cudaMemcpy(q, eidx[t].data(), ne * 4, cudaMemcpyHostToDevice));
-            ed.corr.esc_idx[t] = reinterpret_cast<const uint32_t*>(q);
-            q += (ne * 4 + 8) / 8 * 8;
-            ed.corr.esc_n[t] = (uint32_t)ne;
-            ed.escapes += ne;
+        cudaError_t e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+        int rc = e == cudaSuccess ? exact_tables_build(ed, st) : cuda_fail(e, "cudaStreamCreateWithFlags");
+        if (st) cudaStreamDestroy(st);
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        if (rc) return rc;
+        if (!g_exact_keep_host) {
+            std::vector<double>().swap(g_exact_log);
+            std::vector<double2>().swap(g_exact_sc);
         }
         it = g_exact_corr.emplace(dev, ed).first;
     }
     p.exact = it->second.corr;
     return PRNG_OK;
 }
+
+// The fast fp32 lognormal takes ex2.approx.ftz: results below FLT_MIN would
+// flush to 0.  |z| <= sqrt(-2 ln 2^-24) < 5.78 on the reference's 24-bit
+// grid, so when m - 5.78 s can reach the subnormal range (ln FLT_MIN =
+// -87.34) the request takes the accurate route instead (fp64 exp, one cast:
+// subnormals kept).
+bool logn_fast_ok(double m, double s) { return m - 5.78 * s > -87.0; }
 
 int check_method(int method) {
     if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE)
@@ -583,6 +649,23 @@ int launch_mrg(const uint32_t* s1, const uint32_t* s2, uint64_t n, void* out, co
     return PRNG_OK;
 }
 
+// ---- write-ceiling probe (roofline denominator for write-only kernels) ----
+// The same grid shape and store pattern as the aligned Philox 4-byte body
+// (256-thread CTAs, every SM filled to the unit kernel's occupancy, thread
+// u owning 64 contiguous bytes per grid-stride pass, two 256-bit streaming
+// stores) with no generator work: what HBM takes for pure writes issued
+// this way.
+__global__ void __launch_bounds__(kPhiloxThreads) write_probe_kernel(uint32_t* out, uint64_t groups16) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups16; g += stride) {
+        const uint32_t v = (uint32_t)g;
+        const uint32_t a[4] = {v, v + 1, v + 2, v + 3}, b[4] = {v + 4, v + 5, v + 6, v + 7};
+        const uint32_t c[4] = {v + 8, v + 9, v + 10, v + 11}, d[4] = {v + 12, v + 13, v + 14, v + 15};
+        st_group2(out + 16 * g, a, b);
+        st_group2(out + 16 * g + 8, c, d);
+    }
+}
+
 // ---- elementwise kernels ----
 template <typename T>
 __global__ void range_kernel(T* v, uint64_t n, T scale, T off) {
@@ -646,8 +729,10 @@ int launch_words(const uint32_t* w, uint64_t n, const XformParams& p, void* out,
     void* d = nullptr;
     int rc = bind_output(out, &d);
     if (rc) return rc;
+    int sms = 0;
+    if ((rc = device_sms(&sms))) return rc;
     uint64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > (uint64_t)sms * 16) blocks = (uint64_t)sms * 16;
     words_kernel<X><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(w, n, p, (T*)d);
     PRNG_CUDA(cudaGetLastError());
     return PRNG_OK;
@@ -662,40 +747,104 @@ int launch_range(T* v, uint64_t n, double lo, double hi, void* stream) {
     void* d = nullptr;
     rc = bind_output(v, &d);
     if (rc) return rc;
+    int sms = 0;
+    if ((rc = device_sms(&sms))) return rc;
     uint64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > (uint64_t)sms * 16) blocks = (uint64_t)sms * 16;
     range_kernel<T><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>((T*)d, n, (T)(hi - lo), (T)lo);
     PRNG_CUDA(cudaGetLastError());
     return PRNG_OK;
 }
 
-// ---- library-owned scratch for the host-buffer drop-ins ----
-struct Scratch {
-    void* ptr = nullptr;
-    size_t bytes = 0;
+// ---- library-owned staging for the host-buffer drop-ins ----
+// The plugin drop-ins (prng_kernels_*) hand back ordinary (pageable) host
+// arrays like the reference's _core (_core.pyx:44, 81).  They run a
+// double-buffered pipeline per device: chunk c is generated into device
+// slot c&1 and copied to pinned slot c&1 on a private stream, while the
+// host copies chunk c-1 from pinned memory into the caller's array on
+// several threads -- PCIe, the kernel and the host copy overlap.
+struct Staging {
+    void* dev = nullptr;   // 2 slots of kHostChunk words
+    void* host = nullptr;  // 2 pinned slots
+    size_t slot_bytes = 0;
     cudaStream_t stream = nullptr;
+    cudaEvent_t done[2] = {nullptr, nullptr};
 };
 std::mutex g_scratch_mu;
-std::map<int, Scratch> g_scratch;
+std::map<int, Staging> g_staging;
 
-int scratch(size_t bytes, void** p, cudaStream_t* s) {
+constexpr uint64_t kHostChunk = 1ull << 24;  // words per staged chunk (64 MB)
+
+int staging(size_t slot_bytes, Staging** out) {
     int dev = 0;
     PRNG_CUDA(cudaGetDevice(&dev));
-    Scratch& sc = g_scratch[dev];
-    if (!sc.stream) PRNG_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
-    if (sc.bytes < bytes) {
-        if (sc.ptr) PRNG_CUDA(cudaFree(sc.ptr));
-        sc.ptr = nullptr;
-        sc.bytes = 0;
-        PRNG_CUDA(cudaMalloc(&sc.ptr, bytes));
-        sc.bytes = bytes;
+    Staging& sg = g_staging[dev];
+    if (!sg.stream) {
+        PRNG_CUDA(cudaStreamCreateWithFlags(&sg.stream, cudaStreamNonBlocking));
+        for (auto& e : sg.done) PRNG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    *p = sc.ptr;
-    *s = sc.stream;
+    if (sg.slot_bytes < slot_bytes) {
+        if (sg.dev) PRNG_CUDA(cudaFree(sg.dev));
+        if (sg.host) PRNG_CUDA(cudaFreeHost(sg.host));
+        sg.dev = sg.host = nullptr;
+        sg.slot_bytes = 0;
+        PRNG_CUDA(cudaMalloc(&sg.dev, 2 * slot_bytes));
+        PRNG_CUDA(cudaHostAlloc(&sg.host, 2 * slot_bytes, cudaHostAllocDefault));
+        sg.slot_bytes = slot_bytes;
+    }
+    *out = &sg;
     return PRNG_OK;
 }
 
-constexpr uint64_t kHostChunk = 1ull << 26;  // words per staged chunk
+// memcpy on up to 8 host threads (one pageable destination, pinned source).
+void host_copy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kMinPart = size_t(4) << 20;
+    unsigned nt = std::thread::hardware_concurrency();
+    nt = nt < 1 ? 1 : (nt > 8 ? 8 : nt);
+    if (bytes / kMinPart < nt) nt = (unsigned)(bytes / kMinPart) > 0 ? (unsigned)(bytes / kMinPart) : 1;
+    if (nt == 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t part = (bytes / nt + 63) / 64 * 64;
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < nt; ++t) {
+        const size_t off = part * t;
+        if (off >= bytes) break;
+        const size_t len = bytes - off < part ? bytes - off : part;
+        th.emplace_back([=] { memcpy((char*)dst + off, (const char*)src + off, len); });
+    }
+    memcpy(dst, src, part < bytes ? part : bytes);
+    for (auto& x : th) x.join();
+}
+
+// Runs `gen(done, m, dev_slot, stream)` for consecutive chunks of `n`
+// elements of `esize` bytes and lands them in host_out.
+template <typename Gen>
+int host_pipeline(uint64_t n, size_t esize, void* host_out, Gen&& gen) {
+    if (n == 0) return PRNG_OK;
+    const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
+    Staging* sg = nullptr;
+    int rc = staging(chunk * esize, &sg);
+    if (rc) return rc;
+    const uint64_t nchunks = (n + chunk - 1) / chunk;
+    auto land = [&](uint64_t c) -> int {
+        const uint64_t m = (c + 1) * chunk <= n ? chunk : n - c * chunk;
+        PRNG_CUDA(cudaEventSynchronize(sg->done[c & 1]));
+        host_copy((char*)host_out + c * chunk * esize, (char*)sg->host + (c & 1) * sg->slot_bytes, m * esize);
+        return PRNG_OK;
+    };
+    for (uint64_t c = 0; c < nchunks; ++c) {
+        const uint64_t m = (c + 1) * chunk <= n ? chunk : n - c * chunk;
+        void* d = (char*)sg->dev + (c & 1) * sg->slot_bytes;
+        if ((rc = gen(c * chunk, m, d, sg->stream))) return rc;
+        PRNG_CUDA(cudaMemcpyAsync((char*)sg->host + (c & 1) * sg->slot_bytes, d, m * esize, cudaMemcpyDeviceToHost,
+                                  sg->stream));
+        PRNG_CUDA(cudaEventRecord(sg->done[c & 1], sg->stream));
+        if (c > 0 && (rc = land(c - 1))) return rc;
+    }
+    return land(nchunks - 1);
+}
 
 }  // namespace
 
@@ -708,10 +857,12 @@ const char* prng_last_error(void) { return g_err; }
 #define PHILOX_ARGS uint32_t k0, uint32_t k1, const uint32_t ctr[4], uint32_t lane, uint64_t n
 
 int prng_philox4x32x10_bits(PHILOX_ARGS, uint32_t* out, void* stream) {
+    DeviceGuard guard_;
     return launch_philox<kBits>(k0, k1, ctr, lane, n, out, XformParams{}, stream);
 }
 
 int prng_philox4x32x10_uniform_f32(PHILOX_ARGS, double a, double b, float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_uniform(a, b);
     if (rc) return rc;
     const UniformSpec u = uniform_spec_f32(a, b);
@@ -721,6 +872,7 @@ int prng_philox4x32x10_uniform_f32(PHILOX_ARGS, double a, double b, float* out, 
 }
 
 int prng_philox4x32x10_uniform_f64(PHILOX_ARGS, double a, double b, double* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_uniform(a, b);
     if (rc) return rc;
     const UniformSpec u = uniform_spec_f64(a, b);
@@ -731,6 +883,7 @@ int prng_philox4x32x10_uniform_f64(PHILOX_ARGS, double a, double b, double* out,
 
 int prng_philox4x32x10_gaussian_f32(PHILOX_ARGS, double mean, double stddev, int method, float* out,
                                     void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -747,12 +900,14 @@ int prng_philox4x32x10_gaussian_f32(PHILOX_ARGS, double mean, double stddev, int
 }
 
 int prng_philox4x32x10_gaussian_f64(PHILOX_ARGS, double mean, double stddev, double* out, void* stream) {
+    DeviceGuard guard_;
     return prng_philox4x32x10_gaussian_f64_method(k0, k1, ctr, lane, n, mean, stddev, PRNG_METHOD_ACCURATE, out,
                                                   stream);
 }
 
 int prng_philox4x32x10_gaussian_f64_method(PHILOX_ARGS, double mean, double stddev, int method, double* out,
                                            void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -769,10 +924,12 @@ int prng_philox4x32x10_gaussian_f64_method(PHILOX_ARGS, double mean, double stdd
 
 int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double displ, double scale, int method,
                                      float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_lognormal(m, s, displ, scale);
     if (!rc) rc = check_method(method);
     if (rc) return rc;
     const XformParams p = logn_params(m, s, displ, scale);
+    if (!logn_fast_ok(m, s)) method = PRNG_METHOD_ACCURATE;
     if (method == PRNG_METHOD_FAST && p.ln_scale_f == 1.0f && p.ln_displ_f == 0.0f)  // oneMKL's default form
         return launch_philox<kLognF32FastUnit>(k0, k1, ctr, lane, n, out, p, stream);
     return method == PRNG_METHOD_FAST ? launch_philox<kLognF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
@@ -781,6 +938,7 @@ int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double dis
 
 int prng_philox4x32x10_lognormal_f64(PHILOX_ARGS, double m, double s, double displ, double scale, double* out,
                                      void* stream) {
+    DeviceGuard guard_;
     int rc = check_lognormal(m, s, displ, scale);
     return rc ? rc
               : launch_philox<kLognF64>(k0, k1, ctr, lane, n, out, logn_params(m, s, displ, scale), stream);
@@ -789,10 +947,12 @@ int prng_philox4x32x10_lognormal_f64(PHILOX_ARGS, double m, double s, double dis
 #define MRG_ARGS const uint32_t s1[3], const uint32_t s2[3], uint64_t n
 
 int prng_mrg32k3a_bits(MRG_ARGS, uint32_t* out, void* stream) {
+    DeviceGuard guard_;
     return launch_mrg<kBits>(s1, s2, n, out, XformParams{}, stream);
 }
 
 int prng_mrg32k3a_uniform_f32(MRG_ARGS, double a, double b, float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_uniform(a, b);
     if (rc) return rc;
     const UniformSpec u = uniform_spec_f32(a, b);
@@ -802,6 +962,7 @@ int prng_mrg32k3a_uniform_f32(MRG_ARGS, double a, double b, float* out, void* st
 }
 
 int prng_mrg32k3a_uniform_f64(MRG_ARGS, double a, double b, double* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_uniform(a, b);
     if (rc) return rc;
     const UniformSpec u = uniform_spec_f64(a, b);
@@ -811,6 +972,7 @@ int prng_mrg32k3a_uniform_f64(MRG_ARGS, double a, double b, double* out, void* s
 }
 
 int prng_mrg32k3a_gaussian_f32(MRG_ARGS, double mean, double stddev, int method, float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -827,11 +989,13 @@ int prng_mrg32k3a_gaussian_f32(MRG_ARGS, double mean, double stddev, int method,
 }
 
 int prng_mrg32k3a_gaussian_f64(MRG_ARGS, double mean, double stddev, double* out, void* stream) {
+    DeviceGuard guard_;
     return prng_mrg32k3a_gaussian_f64_method(s1, s2, n, mean, stddev, PRNG_METHOD_ACCURATE, out, stream);
 }
 
 int prng_mrg32k3a_gaussian_f64_method(MRG_ARGS, double mean, double stddev, int method, double* out,
                                       void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -848,16 +1012,19 @@ int prng_mrg32k3a_gaussian_f64_method(MRG_ARGS, double mean, double stddev, int 
 
 int prng_mrg32k3a_lognormal_f32(MRG_ARGS, double m, double s, double displ, double scale, int method, float* out,
                                 void* stream) {
+    DeviceGuard guard_;
     int rc = check_lognormal(m, s, displ, scale);
     if (!rc) rc = check_method(method);
     if (rc) return rc;
     const XformParams p = logn_params(m, s, displ, scale);
+    if (!logn_fast_ok(m, s)) method = PRNG_METHOD_ACCURATE;
     return method == PRNG_METHOD_FAST ? launch_mrg<kLognF32Fast>(s1, s2, n, out, p, stream)
                                       : launch_mrg<kLognF32Accurate>(s1, s2, n, out, p, stream);
 }
 
 int prng_mrg32k3a_lognormal_f64(MRG_ARGS, double m, double s, double displ, double scale, double* out,
                                 void* stream) {
+    DeviceGuard guard_;
     int rc = check_lognormal(m, s, displ, scale);
     return rc ? rc : launch_mrg<kLognF64>(s1, s2, n, out, logn_params(m, s, displ, scale), stream);
 }
@@ -885,15 +1052,18 @@ int prng_mrg32k3a_skip_ahead(const uint32_t s1[3], const uint32_t s2[3], uint64_
 }
 
 int prng_words_to_unit_f32(const uint32_t* words, uint64_t n, float* out, void* stream) {
+    DeviceGuard guard_;
     return launch_words<kUnitF32>(words, n, XformParams{}, out, stream);
 }
 
 int prng_words_to_unit_f64(const uint32_t* words, uint64_t n, double* out, void* stream) {
+    DeviceGuard guard_;
     return launch_words<kUnitF64>(words, n, XformParams{}, out, stream);
 }
 
 int prng_gaussian_from_words_f32(const uint32_t* words, uint64_t n, double mean, double stddev, int method,
                                  float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -909,11 +1079,13 @@ int prng_gaussian_from_words_f32(const uint32_t* words, uint64_t n, double mean,
 
 int prng_gaussian_from_words_f64(const uint32_t* words, uint64_t n, double mean, double stddev, double* out,
                                  void* stream) {
+    DeviceGuard guard_;
     return prng_gaussian_from_words_f64_method(words, n, mean, stddev, PRNG_METHOD_ACCURATE, out, stream);
 }
 
 int prng_gaussian_from_words_f64_method(const uint32_t* words, uint64_t n, double mean, double stddev, int method,
                                         double* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_gaussian(mean, stddev);
     if (!rc) rc = check_gauss_method(method);
     if (rc) return rc;
@@ -927,6 +1099,7 @@ int prng_gaussian_from_words_f64_method(const uint32_t* words, uint64_t n, doubl
 }
 
 int prng_exact_tables_prepare(void) {
+    DeviceGuard guard_;
     XformParams p{};
     return exact_tables(p);
 }
@@ -934,6 +1107,7 @@ int prng_exact_tables_prepare(void) {
 int prng_exact_tables_host(const double** log_table, const double** sincos_table) {
     if (!log_table || !sincos_table) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
     std::lock_guard<std::mutex> lk(g_exact_mu);
+    g_exact_keep_host = true;  // the caller holds the pointers for the life of the process
     if (g_exact_log.empty()) build_exact_host_tables();
     *log_table = g_exact_log.data();
     *sincos_table = reinterpret_cast<const double*>(g_exact_sc.data());
@@ -941,15 +1115,18 @@ int prng_exact_tables_host(const double** log_table, const double** sincos_table
 }
 
 int prng_range_transform_f32(float* values, uint64_t n, double lo, double hi, void* stream) {
+    DeviceGuard guard_;
     return launch_range<float>(values, n, lo, hi, stream);
 }
 
 int prng_range_transform_f64(double* values, uint64_t n, double lo, double hi, void* stream) {
+    DeviceGuard guard_;
     return launch_range<double>(values, n, lo, hi, stream);
 }
 
 int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng_segment_t* segs, uint32_t nseg,
                                             uint64_t max_count, double a, double b, float* out, void* stream) {
+    DeviceGuard guard_;
     int rc = check_uniform(a, b);
     if (rc) return rc;
     if (nseg == 0 || max_count == 0) return PRNG_OK;
@@ -979,58 +1156,63 @@ int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng
     return PRNG_OK;
 }
 
+int prng_diag_write_probe(void* out, uint64_t bytes, void* stream) {
+    DeviceGuard guard_;
+    if (!out || ((uintptr_t)out & 31u) || (bytes & 63u))
+        return fail(PRNG_ERR_INVALID_PARAMETER, "write probe needs a 32-byte aligned buffer of 64-byte multiples");
+    void* d = nullptr;
+    int rc = bind_output(out, &d);
+    if (rc) return rc;
+    int sms = 0, occ = 0;
+    if ((rc = resident_ctas((const void*)philox_kernel<kUnitF32, 0>, kPhiloxThreads, &sms, &occ))) return rc;
+    const uint64_t groups = bytes / 64;
+    uint64_t blocks = (groups + kPhiloxThreads - 1) / kPhiloxThreads;
+    if (blocks > (uint64_t)sms * occ) blocks = (uint64_t)sms * occ;
+    if (blocks < 1) blocks = 1;
+    write_probe_kernel<<<(unsigned)blocks, kPhiloxThreads, 0, (cudaStream_t)stream>>>((uint32_t*)d, groups);
+    PRNG_CUDA(cudaGetLastError());
+    return PRNG_OK;
+}
+
 int prng_kernels_philox_fill(uint32_t k0, uint32_t k1, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3,
                              uint32_t offset, uint64_t n, uint32_t* host_out) {
+    DeviceGuard guard_;
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     if (n == 0) return PRNG_OK;
     if (!host_out) return fail(PRNG_ERR_INVALID_PARAMETER, "host_out must not be NULL");
-    if (offset > 3) return fail(PRNG_ERR_INVALID_PARAMETER, "offset must be 0..3, got %u", offset);
-    void* d = nullptr;
-    cudaStream_t s = nullptr;
-    const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
-    int rc = scratch(chunk * 4, &d, &s);
-    if (rc) return rc;
+    // _core.pyx:49-62: `lane = offset`; a lane >= 4 emits nothing from the
+    // first block, then the counter steps and lane restarts at 0 -- so any
+    // offset >= 4 streams from block b + 1, word 0.
+    u128 base_blk = ((u128)b3 << 96) | ((u128)b2 << 64) | ((u128)b1 << 32) | b0;
+    if (offset > 3) {
+        base_blk += 1;
+        offset = 0;
+    }
     // Each chunk restarts from its own stream offset exactly as the
     // reference's chunk kernels do (rngburn.py:70-73); the block counter
     // wraps mod 2^128 like _core.pyx:63-70.
-    const u128 base_blk = ((u128)b3 << 96) | ((u128)b2 << 64) | ((u128)b1 << 32) | b0;
-    for (uint64_t done = 0; done < n; done += chunk) {
-        const uint64_t m = (n - done) < chunk ? (n - done) : chunk;
+    return host_pipeline(n, 4, host_out, [&](uint64_t done, uint64_t m, void* d, cudaStream_t s) {
         const uint64_t rel = (uint64_t)offset + done;
         const u128 blk = base_blk + (rel >> 2);
         const uint32_t ctr[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), (uint32_t)(blk >> 64), (uint32_t)(blk >> 96)};
-        rc = launch_philox<kBits>(k0, k1, ctr, (uint32_t)(rel & 3), m, d, XformParams{}, s);
-        if (rc) return rc;
-        PRNG_CUDA(cudaMemcpyAsync(host_out + done, d, m * 4, cudaMemcpyDeviceToHost, s));
-    }
-    PRNG_CUDA(cudaStreamSynchronize(s));
-    return PRNG_OK;
+        return launch_philox<kBits>(k0, k1, ctr, (uint32_t)(rel & 3), m, d, XformParams{}, s);
+    });
 }
 
 int prng_kernels_mrg_fill(uint32_t s10, uint32_t s11, uint32_t s12, uint32_t s20, uint32_t s21, uint32_t s22,
                           uint64_t n, uint32_t* host_out, uint32_t s1_out[3], uint32_t s2_out[3]) {
+    DeviceGuard guard_;
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     uint32_t s1[3] = {s10, s11, s12}, s2[3] = {s20, s21, s22};
     int rc = check_mrg_state(s1, s2);
     if (rc) return rc;
     if (n && !host_out) return fail(PRNG_ERR_INVALID_PARAMETER, "host_out must not be NULL");
-    void* d = nullptr;
-    cudaStream_t s = nullptr;
-    const uint64_t chunk = n < kHostChunk ? n : kHostChunk;
-    if (n) {
-        rc = scratch(chunk * 4, &d, &s);
-        if (rc) return rc;
-    }
     uint32_t c1[3] = {s10, s11, s12}, c2[3] = {s20, s21, s22};
-    for (uint64_t done = 0; done < n; done += chunk) {
-        const uint64_t m = (n - done) < chunk ? (n - done) : chunk;
-        rc = launch_mrg<kBits>(c1, c2, m, d, XformParams{}, s);
-        if (rc) return rc;
-        PRNG_CUDA(cudaMemcpyAsync(host_out + done, d, m * 4, cudaMemcpyDeviceToHost, s));
-        rc = prng_mrg32k3a_skip_ahead(c1, c2, m, 0, c1, c2);
-        if (rc) return rc;
-    }
-    if (n) PRNG_CUDA(cudaStreamSynchronize(s));
+    rc = host_pipeline(n, 4, host_out, [&](uint64_t, uint64_t m, void* d, cudaStream_t s) {
+        int r = launch_mrg<kBits>(c1, c2, m, d, XformParams{}, s);
+        return r ? r : prng_mrg32k3a_skip_ahead(c1, c2, m, 0, c1, c2);
+    });
+    if (rc) return rc;
     if (s1_out && s2_out)
         for (int i = 0; i < 3; ++i) {
             s1_out[i] = c1[i];
@@ -1040,21 +1222,24 @@ int prng_kernels_mrg_fill(uint32_t s10, uint32_t s11, uint32_t s12, uint32_t s20
 }
 
 int prng_kernels_box_muller(const double* u1, const double* u2, uint64_t m, double* z0, double* z1) {
+    DeviceGuard guard_;
     std::lock_guard<std::mutex> lk(g_scratch_mu);
     if (m == 0) return PRNG_OK;
     if (!u1 || !u2 || !z0 || !z1) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL array");
-    void* d = nullptr;
-    cudaStream_t s = nullptr;
-    int rc = scratch(m * 32, &d, &s);
+    Staging* sg = nullptr;
+    int rc = staging(m * 16, &sg);  // two slots: (u1, u2) and (z0, z1)
     if (rc) return rc;
-    double* du1 = (double*)d;
+    cudaStream_t s = sg->stream;
+    double* du1 = (double*)sg->dev;
     double* du2 = du1 + m;
     double* dz0 = du2 + m;
     double* dz1 = dz0 + m;
     PRNG_CUDA(cudaMemcpyAsync(du1, u1, m * 8, cudaMemcpyHostToDevice, s));
     PRNG_CUDA(cudaMemcpyAsync(du2, u2, m * 8, cudaMemcpyHostToDevice, s));
+    int sms = 0;
+    if ((rc = device_sms(&sms))) return rc;
     uint64_t blocks = (m + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
     XformParams p{};
     if ((rc = exact_tables(p))) return rc;
     box_muller_kernel<<<(unsigned)blocks, 256, 0, s>>>(du1, du2, m, dz0, dz1, p);

@@ -452,7 +452,8 @@ def gaussian_generate_kernel(base_state: EngineState, buf_id: int, mean: float, 
             return
         first_pair = start // 2
         state = skip_ahead(base_state, 2 * first_pair)
-        _, tmp = generate(spec, state, stop - 2 * first_pair)
+        _, tmp = generate(spec, state, stop - 2 * first_pair,
+                          out=_torch().empty(stop - 2 * first_pair, dtype=out.dtype, device=out.device))
         out[start:stop].copy_(tmp[1:])
 
     return kernel

@@ -14,7 +14,7 @@ Two strategies, both a single pass over HBM or none at all:
 from __future__ import annotations
 
 from .distributions import DistributionSpec, Gaussian, Lognormal, generate, out_dtype, words_consumed
-from .engine import EngineState, _torch, skip_ahead
+from .engine import EngineState, Mrg32k3a, Philox4x32x10, _torch, skip_ahead
 from .errors import InvalidParameter
 
 _CHUNK = 1 << 25
@@ -40,11 +40,21 @@ class HostGenerator:
         return self._bufs[dtype]
 
     def generate(self, spec: DistributionSpec, state: EngineState, n: int, host_out):
-        """Fill host_out[:n] (pinned CPU tensor); returns the advanced state.
-        Work is enqueued on this generator's streams; call synchronize()."""
+        """Fill host_out[:n] (pinned CPU tensor); returns the advanced state
+        (a stateful Philox4x32x10 / Mrg32k3a engine is advanced in place and
+        returned).  Work is enqueued on this generator's streams; call
+        synchronize()."""
         torch = _torch()
         if host_out.is_cuda or not host_out.is_pinned():
             raise InvalidParameter("host_out must be a pinned CPU tensor")
+        if n < 0:
+            raise InvalidParameter("count must be non-negative")
+        if isinstance(state, (Philox4x32x10, Mrg32k3a)):
+            # validate and enqueue on the immutable state first; advance the
+            # engine object only once every chunk is enqueued
+            engine = state
+            self.generate(spec, engine.state, n, host_out)
+            return engine.skip_ahead(words_consumed(spec, n))
         if self.strategy == "zero_copy":
             s = self.streams[0]
             generate(spec, state, n, out=host_out, stream=s)

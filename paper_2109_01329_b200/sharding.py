@@ -13,7 +13,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from .distributions import DistributionSpec, Gaussian, Lognormal, generate, words_consumed
-from .engine import EngineState, skip_ahead
+from .engine import EngineState, Mrg32k3a, Philox4x32x10, skip_ahead
 
 
 @dataclass(frozen=True)
@@ -46,7 +46,10 @@ def weak_shard(n_per_rank: int, rank: int, world: int) -> Shard:
 
 
 def shard_state(spec: DistributionSpec, base: EngineState, shard: Shard) -> EngineState:
-    """Engine state at the shard's first element (pairs count 2 words per 2 samples)."""
+    """Engine state at the shard's first element (pairs count 2 words per 2 samples).
+    A stateful engine object is read, not advanced."""
+    if isinstance(base, (Philox4x32x10, Mrg32k3a)):
+        base = base.state
     if isinstance(spec, (Gaussian, Lognormal)) and shard.start % 2:
         raise ValueError("gaussian/lognormal shards must start on an even element")
     return skip_ahead(base, words_consumed(spec, shard.start) if shard.start else 0)
