@@ -415,8 +415,14 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
     s.n = n;
     uint64_t i0 = ((32u - (uint32_t)((uintptr_t)dptr & 31u)) & 31u) / sizeof(T);
     uint64_t ngroups = 0;
-    if ((kPair && (i0 & 1)) || i0 >= n) {
-        i0 = n;  // misaligned for pairs (or tiny): everything scalar
+    // Pair transforms need groups that start on a pair boundary: with an odd
+    // head (an odd-element output view) the body starts one element early,
+    // one element below the 32-byte boundary, and each group is stored as
+    // element + aligned pair + element (PhiloxBody::mis).
+    const uint32_t mis = (kPair && (i0 & 1)) ? 1u : 0u;
+    i0 -= mis;
+    if (i0 >= n) {
+        i0 = n;  // tiny: everything scalar
     } else {
         ngroups = (n - i0) >> 2;
     }
@@ -444,7 +450,7 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
         // A launch boundary at an odd group leaves the next body 16-byte
         // aligned; emit one single-group launch to restore 32-byte alignment
         // for the 256-bit stores (rare: only at 2^34-word stream boundaries).
-        if (left > 0 && ((uintptr_t)body & 31u) != 0) g = 1;
+        if (left > 0 && ((uintptr_t)(body + mis) & 31u) != 0) g = 1;
         PhiloxBody a{};
         a.k0 = k0;
         a.k1 = k1;
@@ -453,6 +459,7 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
         a.c2 = (uint32_t)(blk >> 64);
         a.c3 = (uint32_t)(blk >> 96);
         a.ngroups = (uint32_t)g;
+        a.mis = mis;
         a.pre = philox_pre(k0, k1, a.c1, a.c2, a.c3);
         a.out = body;
         a.p = p;

@@ -48,6 +48,7 @@ struct PhiloxBody {
     uint32_t k0, k1;
     uint32_t c0, c1, c2, c3;
     uint32_t ngroups;
+    uint32_t mis;  // pair transforms at an odd-element output: body = 32-byte boundary - 1 element
     PhiloxPre pre;  // philox_pre(k0, k1, c1, c2, c3)
     void* out;  // address of group 0
     XformParams p;
@@ -125,41 +126,75 @@ constexpr bool philox_pipelined() {
 }
 template <> struct PhiloxBpt<double> { static constexpr int kValue = 2; };
 
-template <int X, int SHIFT>
-__device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, uint32_t gstride) {
+// Store of one group whose first element sits one element below a 32-byte
+// boundary (pair transforms into an odd-element output view, PhiloxBody::mis):
+// the pairs keep their natural grouping, and the group goes out as element,
+// aligned pair, element.
+template <typename T>
+__device__ __forceinline__ void st_group_mis(T* p, const T o[4]) {
+    if constexpr (sizeof(T) == 4) {
+        uint32_t b[4];
+        memcpy(b, o, 16);
+        asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(b[0]) : "memory");
+        asm volatile("st.global.cs.v2.b32 [%0], {%1,%2};" ::"l"(p + 1), "r"(b[1]), "r"(b[2]) : "memory");
+        asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p + 3), "r"(b[3]) : "memory");
+    } else {
+        unsigned long long b[4];
+        memcpy(b, o, 32);
+        asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(b[0]) : "memory");
+        asm volatile("st.global.cs.v2.b64 [%0], {%1,%2};" ::"l"(p + 1), "l"(b[1]), "l"(b[2]) : "memory");
+        asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p + 3), "l"(b[3]) : "memory");
+    }
+}
+
+// Aligned path (SHIFT = 0) of one body launch; MIS: pair transforms whose
+// body starts one element below a 32-byte boundary (a separate instantiation
+// so the common loop keeps its register allocation).
+template <int X, bool MIS>
+__device__ __forceinline__ void philox_body_aligned(const PhiloxBody& a, uint32_t gtid, uint32_t gstride) {
     using T = typename XformTraits<X>::T;
     T* __restrict__ body = static_cast<T*>(a.out);
-    if constexpr (SHIFT == 0) {
-        constexpr int BPT = PhiloxBpt<T>::kValue;
-        // Running group index and output pointer (adds on the ALU pipe; the
-        // FMA-heavy pipe is kept for the Philox multiplies).
-        // The steady-state loop covers whole units only (no per-iteration
-        // bounds branch); the < BPT leftover groups go to one thread after it.
-        const uint32_t gstep = gstride * BPT;
-        const uint32_t gfull = a.ngroups - a.ngroups % BPT;
-        T* dst = body + (size_t)4 * BPT * gtid;
-        if constexpr (philox_pipelined<X>()) {
-            // Software-pipelined: the next pass's Philox blocks (FMA-heavy
-            // IMAD.WIDE + ALU) are computed in the same basic block as this
-            // pass's transform (FMA-lite, XU, LSU), so the scheduler can
-            // interleave the two instruction mixes.  The blocks computed on
-            // the last pass are not used (counter wrap is harmless there).
-            U4 w[BPT];
+    constexpr int BPT = PhiloxBpt<T>::kValue;
+    // Running group index and output pointer (adds on the ALU pipe; the
+    // FMA-heavy pipe is kept for the Philox multiplies).
+    // The steady-state loop covers whole units only (no per-iteration
+    // bounds branch); the < BPT leftover groups go to one thread after it.
+    const uint32_t gstep = gstride * BPT;
+    const uint32_t gfull = a.ngroups - a.ngroups % BPT;
+    T* dst = body + (size_t)4 * BPT * gtid;
+    auto store = [&](T* d, T (&o)[BPT][4]) {
+        if constexpr (MIS) {
 #pragma unroll
-            for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre(a.k0, a.k1, a.c0 + gtid * BPT + j, a.pre);
-            for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
-                U4 nw[BPT];
+            for (int j = 0; j < BPT; ++j) st_group_mis(d + 4 * j, o[j]);
+        } else if constexpr (sizeof(T) == 4) {
 #pragma unroll
-                for (int j = 0; j < BPT; ++j) nw[j] = philox_block_pre(a.k0, a.k1, a.c0 + g0 + gstep + j, a.pre);
-                T o[BPT][4];
+            for (int j = 0; j < BPT; j += 2) st_group2(d + 4 * j, o[j], o[j + 1]);
+        } else {
 #pragma unroll
-                for (int j = 0; j < BPT; ++j) xform4<X>(w[j], a.p, o[j]);
+            for (int j = 0; j < BPT; ++j) st_group(d + 4 * j, o[j]);
+        }
+    };
+    if constexpr (philox_pipelined<X>()) {
+        // Software-pipelined: the next pass's Philox blocks (FMA-heavy
+        // IMAD.WIDE + ALU) are computed in the same basic block as this
+        // pass's transform (FMA-lite, XU, LSU), so the scheduler can
+        // interleave the two instruction mixes.  The blocks computed on
+        // the last pass are not used (counter wrap is harmless there).
+        U4 w[BPT];
 #pragma unroll
-                for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
+        for (int j = 0; j < BPT; ++j) w[j] = philox_block_pre(a.k0, a.k1, a.c0 + gtid * BPT + j, a.pre);
+        for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
+            U4 nw[BPT];
 #pragma unroll
-                for (int j = 0; j < BPT; ++j) w[j] = nw[j];
-            }
-        } else
+            for (int j = 0; j < BPT; ++j) nw[j] = philox_block_pre(a.k0, a.k1, a.c0 + g0 + gstep + j, a.pre);
+            T o[BPT][4];
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) xform4<X>(w[j], a.p, o[j]);
+            store(dst, o);
+#pragma unroll
+            for (int j = 0; j < BPT; ++j) w[j] = nw[j];
+        }
+    } else {
         for (uint32_t g0 = gtid * BPT; g0 < gfull; g0 += gstep, dst += (size_t)4 * gstep) {
             T o[BPT][4];
 #pragma unroll
@@ -167,21 +202,33 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
                 const U4 w = philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + g0 + j, a.pre);
                 xform4<X>(w, a.p, o[j]);
             }
-            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                for (int j = 0; j < BPT; j += 2) st_group2(dst + 4 * j, o[j], o[j + 1]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < BPT; ++j) st_group(dst + 4 * j, o[j]);
-            }
+            store(dst, o);
         }
-        if (gtid == gstride - 1) {
-            for (uint32_t g = gfull; g < a.ngroups; ++g) {
-                T o[4];
-                xform4<X>(philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + g, a.pre), a.p, o);
+    }
+    if (gtid == gstride - 1) {
+        for (uint32_t g = gfull; g < a.ngroups; ++g) {
+            T o[4];
+            xform4<X>(philox_block_pre<philox_rk<X>()>(a.k0, a.k1, a.c0 + g, a.pre), a.p, o);
+            if constexpr (MIS)
+                st_group_mis(body + (size_t)4 * g, o);
+            else
                 st_group(body + (size_t)4 * g, o);
+        }
+    }
+}
+
+template <int X, int SHIFT>
+__device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, uint32_t gstride) {
+    using T = typename XformTraits<X>::T;
+    T* __restrict__ body = static_cast<T*>(a.out);
+    if constexpr (SHIFT == 0) {
+        if constexpr (XformTraits<X>::kPair) {
+            if (a.mis) {
+                philox_body_aligned<X, true>(a, gtid, gstride);
+                return;
             }
         }
+        philox_body_aligned<X, false>(a, gtid, gstride);
     } else {
         // Warp-cooperative funnel.  Lane l of a warp pass computes blocks
         // 4l..4l+3 of the tile and takes block 4l+4 (the first block of lane
@@ -220,7 +267,11 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             for (int j = 0; j < BPT; ++j) xform4<X>(funnel<SHIFT>(w[j], w[j + 1]), a.p, o[j]);
             T* dst = body + (size_t)4 * gb;
             const uint32_t nvalid = lane == 31 ? 2 : BPT;  // groups of this lane inside the pass
-            if (nvalid == BPT && gb + BPT <= a.ngroups) {
+            if (XformTraits<X>::kPair && a.mis != 0u) {
+#pragma unroll
+                for (int j = 0; j < BPT; ++j)
+                    if (j < (int)nvalid && gb + j < a.ngroups) st_group_mis(dst + 4 * j, o[j]);
+            } else if (nvalid == BPT && gb + BPT <= a.ngroups) {
                 if constexpr (sizeof(T) == 4) {
                     st_group2(dst, o[0], o[1]);
                     st_group2(dst + 8, o[2], o[3]);
@@ -283,6 +334,7 @@ __global__ void __launch_bounds__(kPhiloxThreads)
     for (uint32_t s = blockIdx.y; s < nseg; s += gridDim.y) {
         const PhiloxSegment sg = segs[s];
         PhiloxBody a;
+        a.mis = 0u;
         a.k0 = k0;
         a.k1 = k1;
         a.p = p;

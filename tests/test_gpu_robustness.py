@@ -138,7 +138,8 @@ def test_lognormal_fp32_keeps_subnormal_results(m, s):
     want = O.generate("philox", (O.seed_philox(777), 0), "lognormal", n, "fp32", m, s)
     got = x.cpu().numpy()
     if m == -100.0:
-        assert (want < np.finfo(np.float32).tiny).all() and (want > 0).all()  # all subnormal
+        # every value is subnormal or underflows to 0 in fp32; most are subnormal
+        assert (want < np.finfo(np.float32).tiny).all() and (want > 0).mean() > 0.9
     # m - 5.78 s < -87: the library routes the request to the accurate path (1 ulp)
     check_close(got, want, lognormal_allowed(want, m, s, np.float32, False), "lognormal subnormal range")
     assert np.array_equal(got == 0, want == 0)
