@@ -49,6 +49,12 @@ WORKLOADS = {
     "c2": ("mrg", "uniform", "fp64", 1 << 28, "mrg32k3a seed=777 uniform fp64 [-1,1) (C2)"),
     "c3_gauss": ("philox", "gaussian", "fp32", 1 << 30, "philox4x32x10 seed=777 gaussian fp32 (0,1) (C3)"),
     "c3_logn": ("philox", "lognormal", "fp32", 1 << 30, "philox4x32x10 seed=777 lognormal fp32 (0,1) (C3)"),
+    "c3_gauss_precise": ("philox", "gaussian", "fp32", 1 << 30,
+                         "philox4x32x10 seed=777 gaussian fp32 (0,1) method=precise (C3)"),
+    "c3_logn_precise": ("philox", "lognormal", "fp32", 1 << 30,
+                        "philox4x32x10 seed=777 lognormal fp32 (0,1) method=precise (C3)"),
+    "c3_gauss_exact": ("philox", "gaussian", "fp32", 1 << 30,
+                       "philox4x32x10 seed=777 gaussian fp32 (0,1) method=exact (C3, bit-exact)"),
     "c5": ("philox", "uniform", "fp32", 0, "FastCaloSim-style ~10^4 x 200k fp32 batches (C5)"),
     "c5_full": ("philox", "uniform", "fp32", 0, "FastCaloSim single-electron run incl. deposition (C5)"),
 }
@@ -60,6 +66,11 @@ KERNEL_NAMES = {
     "c2": "mrg_kernel<kUniformF64>",
     "c3_gauss": "philox_kernel<kGaussF32Fast, SHIFT=0>",
     "c3_logn": "philox_kernel<kLognF32FastUnit, SHIFT=0>",
+    "c3_gauss_precise": "philox_kernel<kGaussF32Precise, SHIFT=0>",
+    "c3_logn_precise": "philox_kernel<kLognF32Precise, SHIFT=0>",
+    "c3_gauss_exact": "philox_kernel<kGaussF32Exact, SHIFT=0>",
+}
+WORKLOAD_METHOD = {"c3_gauss_precise": "precise", "c3_logn_precise": "precise", "c3_gauss_exact": "exact",
 }
 
 
@@ -121,9 +132,9 @@ def slice_check(P, torch, workload, spec, out, n, rank):
             ok &= bool(np.array_equal(got, want))
         else:
             dt = np.float32 if prec == "fp32" else np.float64
-            fast = getattr(spec, "method", "fast") == "fast"
-            allowed = (TOL.gaussian_allowed(want, 0.0, 1.0, dt, fast) if dist == "gaussian"
-                       else TOL.lognormal_allowed(want, 0.0, 1.0, dt, fast))
+            method = getattr(spec, "method", "fast")
+            allowed = (TOL.gaussian_allowed(want, 0.0, 1.0, dt, method) if dist == "gaussian"
+                       else TOL.lognormal_allowed(want, 0.0, 1.0, dt, method))
             err = np.abs(got.astype(np.float64) - want.astype(np.float64))
             ok &= bool(np.all(err <= allowed))
             worst = max(worst, float(np.max(err / allowed)))
@@ -146,14 +157,14 @@ def host_mem_available():
     return 0
 
 
-def make_spec(P, dist, prec):
+def make_spec(P, dist, prec, method="fast"):
     if dist == "bits":
         return P.UniformBits()
     if dist == "uniform":
         return P.Uniform(-1.0, 1.0, prec) if prec == "fp64" else P.Uniform(0.0, 1.0, prec)
     if dist == "gaussian":
-        return P.Gaussian(0.0, 1.0, prec)
-    return P.Lognormal(0.0, 1.0, precision=prec)
+        return P.Gaussian(0.0, 1.0, prec, method)
+    return P.Lognormal(0.0, 1.0, precision=prec, method=method)
 
 
 class ClockSampler:
@@ -698,7 +709,7 @@ def run_ours(args):
 
     engine, dist, prec, n_default, desc = WORKLOADS[args.workload]
     n = args.n or n_default
-    spec = make_spec(P, dist, prec)
+    spec = make_spec(P, dist, prec, WORKLOAD_METHOD.get(args.workload, "fast"))
     base = P.seed_engine(P.EngineKind.PHILOX4X32X10 if engine == "philox" else P.EngineKind.MRG32K3A, 777)
     shard = weak_shard(n, rank, world)
     st = shard_state(spec, base, shard)

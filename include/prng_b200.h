@@ -65,6 +65,15 @@ extern "C" {
  * a first exact request inside CUDA-graph capture works; it blocks the
  * calling thread for about a second. */
 #define PRNG_METHOD_EXACT 2
+/* fp32 gaussian / lognormal: relative accuracy everywhere at ~85% of FAST's
+ * throughput -- -lg2(1 - u1) from a 12 KB table over the bits of 1 - u1 plus
+ * a 4-term series (no SFU log), sqrt.approx, and sin/cos from the nearest
+ * point of a 4096-entry table with the x^2 term.  Gaussian within 5 ulp of
+ * the reference for every input (exhaustive over both 24-bit grids),
+ * lognormal within 5 ulp * max(1, |ln x|).  MRG32k3a
+ * requests take ACCURATE (its kernel's shared memory holds the store stage);
+ * fp64 outputs take ACCURATE. */
+#define PRNG_METHOD_PRECISE 3
 
 int prng_abi_version(void);
 const char *prng_last_error(void);
@@ -141,6 +150,12 @@ int prng_gaussian_from_words_f64_method(const uint32_t *words, uint64_t n, doubl
  * fl(TWO_PI k 2^-24)) for inspection. */
 int prng_exact_tables_prepare(void);
 int prng_exact_tables_host(const double **log_table, const double **sincos_table);
+/* The current device's exact tables (built if needed): worst relative error
+ * of the device log approximation and worst absolute error of its sin/cos
+ * against the host libm over the whole domains (bounds[0], bounds[1]) --
+ * the fp32 exact route's rounding test uses them -- and the number of
+ * escape-list entries. */
+int prng_exact_tables_bounds(double bounds[2], uint64_t *escapes);
 
 /* ---- Many small batches (FastCaloSim consumer, calosim.py:269-358). ----
  * One launch generates every segment: segment i writes `count` fp32 uniforms

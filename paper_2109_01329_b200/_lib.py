@@ -28,6 +28,7 @@ PRNG_ERR_CUDA = -5
 METHOD_FAST = 0
 METHOD_ACCURATE = 1
 METHOD_EXACT = 2
+METHOD_PRECISE = 3
 
 _u32 = ctypes.c_uint32
 _u64 = ctypes.c_uint64
@@ -68,6 +69,7 @@ SIGNATURES = {
     "prng_gaussian_from_words_f64_method": ([_vp, _u64, _dbl, _dbl, _int, _vp, _vp], _int),
     "prng_exact_tables_prepare": ([], _int),
     "prng_exact_tables_host": ([ctypes.POINTER(ctypes.POINTER(ctypes.c_double))] * 2, _int),
+    "prng_exact_tables_bounds": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_uint64)], _int),
     "prng_philox4x32x10_uniform_f32_segments": ([_u32, _u32, _vp, _u32, _u64, _dbl, _dbl, _vp, _vp], _int),
     "prng_calo_hits": ([_vp, _vp, _u32, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     "prng_calo_deposit_scratch_bytes": ([_u64, _u32], ctypes.c_size_t),

@@ -6,6 +6,7 @@
 // device path allocates memory or synchronises the host.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -157,8 +158,9 @@ int check_lognormal(double m, double s, double displ, double scale) {
 }
 
 int check_gauss_method(int method) {
-    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE && method != PRNG_METHOD_EXACT)
-        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST, _ACCURATE or _EXACT");
+    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE && method != PRNG_METHOD_EXACT &&
+        method != PRNG_METHOD_PRECISE)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST, _ACCURATE, _EXACT or _PRECISE");
     return PRNG_OK;
 }
 
@@ -249,6 +251,21 @@ int exact_tables_build(ExactDevice& ed, cudaStream_t st) {
         lnib[i / 2] = (uint8_t)(nibble(g_exact_log[i], aL[i]) | (nibble(g_exact_log[i + 1], aL[i + 1]) << 4));
     for (size_t i = 0; i < kExactN; ++i)
         scnib[i] = (uint8_t)(nibble(g_exact_sc[i].x, aS[i]) | (nibble(g_exact_sc[i].y, aC[i]) << 4));
+    // worst approximation errors (the fp32 route's rounding test): relative
+    // for the log (0 only at u1' = 1, where both are exactly 0), absolute for
+    // sin / cos
+    double rel_log = 0.0, abs_sc = 0.0;
+    for (size_t i = 0; i < kExactN; ++i) {
+        const double w = g_exact_log[i], a = aL[i];
+        if (w == 0.0) {
+            if (a != 0.0) rel_log = INFINITY;
+        } else {
+            rel_log = std::max(rel_log, std::fabs(a - w) / std::fabs(w));
+        }
+        abs_sc = std::max(abs_sc, std::max(std::fabs(aS[i] - g_exact_sc[i].x), std::fabs(aC[i] - g_exact_sc[i].y)));
+    }
+    ed.corr.rel_log = rel_log;
+    ed.corr.abs_sc = abs_sc;
     std::vector<uint32_t> eidx[3];
     std::vector<double> eval[3];
     for (size_t i = 0; i < kExactN; ++i) {
@@ -325,8 +342,8 @@ int exact_tables(XformParams& p) {
 bool logn_fast_ok(double m, double s) { return m - 5.78 * s > -87.0; }
 
 int check_method(int method) {
-    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE)
-        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST or PRNG_METHOD_ACCURATE");
+    if (method != PRNG_METHOD_FAST && method != PRNG_METHOD_ACCURATE && method != PRNG_METHOD_PRECISE)
+        return fail(PRNG_ERR_INVALID_PARAMETER, "method must be PRNG_METHOD_FAST, _ACCURATE or _PRECISE");
     return PRNG_OK;
 }
 
@@ -902,6 +919,7 @@ int prng_philox4x32x10_gaussian_f32(PHILOX_ARGS, double mean, double stddev, int
         if ((rc = bind_output(out, &d)) || (rc = exact_tables(p))) return rc;
         return launch_philox<kGaussF32Exact>(k0, k1, ctr, lane, n, out, p, stream);
     }
+    if (method == PRNG_METHOD_PRECISE) return launch_philox<kGaussF32Precise>(k0, k1, ctr, lane, n, out, p, stream);
     return method == PRNG_METHOD_FAST ? launch_philox<kGaussF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
                                       : launch_philox<kGaussF32Accurate>(k0, k1, ctr, lane, n, out, p, stream);
 }
@@ -937,6 +955,7 @@ int prng_philox4x32x10_lognormal_f32(PHILOX_ARGS, double m, double s, double dis
     if (rc) return rc;
     const XformParams p = logn_params(m, s, displ, scale);
     if (!logn_fast_ok(m, s)) method = PRNG_METHOD_ACCURATE;
+    if (method == PRNG_METHOD_PRECISE) return launch_philox<kLognF32Precise>(k0, k1, ctr, lane, n, out, p, stream);
     if (method == PRNG_METHOD_FAST && p.ln_scale_f == 1.0f && p.ln_displ_f == 0.0f)  // oneMKL's default form
         return launch_philox<kLognF32FastUnit>(k0, k1, ctr, lane, n, out, p, stream);
     return method == PRNG_METHOD_FAST ? launch_philox<kLognF32Fast>(k0, k1, ctr, lane, n, out, p, stream)
@@ -1080,6 +1099,7 @@ int prng_gaussian_from_words_f32(const uint32_t* words, uint64_t n, double mean,
         if ((rc = exact_tables(p))) return rc;
         return launch_words<kGaussF32Exact>(words, n, p, out, stream);
     }
+    if (method == PRNG_METHOD_PRECISE) return launch_words<kGaussF32Precise>(words, n, p, out, stream);
     return method == PRNG_METHOD_FAST ? launch_words<kGaussF32Fast>(words, n, p, out, stream)
                                       : launch_words<kGaussF32Accurate>(words, n, p, out, stream);
 }
@@ -1109,6 +1129,18 @@ int prng_exact_tables_prepare(void) {
     DeviceGuard guard_;
     XformParams p{};
     return exact_tables(p);
+}
+
+int prng_exact_tables_bounds(double bounds[2], uint64_t* escapes) {
+    DeviceGuard guard_;
+    if (!bounds || !escapes) return fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
+    XformParams p{};
+    int rc = exact_tables(p);
+    if (rc) return rc;
+    bounds[0] = p.exact.rel_log;
+    bounds[1] = p.exact.abs_sc;
+    *escapes = (uint64_t)p.exact.esc_n[0] + p.exact.esc_n[1] + p.exact.esc_n[2];
+    return PRNG_OK;
 }
 
 int prng_exact_tables_host(const double** log_table, const double** sincos_table) {

@@ -219,6 +219,12 @@ struct ExactCorrections {
     const uint32_t* esc_idx[3];  // escapes (correction -8): sorted indices ...
     const double* esc_val[3];    // ... and the host-libm values; [0] log, [1] sin, [2] cos
     uint32_t esc_n[3];
+    // Worst differences of the approximations from the host libm over the
+    // whole domains (measured when the tables are built): relative for
+    // log_u1_f64, absolute for sincos_ref_f64.  The fp32 exact route uses
+    // them to decide when the uncorrected value already rounds like the
+    // reference's (box_muller_f32_exact).
+    double rel_log, abs_sc;
 };
 
 // Parameters of one fused request.  For uniform: (a, b) -> scale/offset with
@@ -249,9 +255,14 @@ enum Xform : int {
     kGaussF32Exact = 11,  // the reference's fp64 Box-Muller bit for bit, cast once
     kGaussF64Exact = 12,
     kLognF32FastUnit = 13,  // kLognF32Fast with scale 1, displ 0 (no final affine: bit-identical)
+    kGaussF32Precise = 14,  // fp32 route with relative accuracy everywhere (table log, centred sin/cos + x^2)
+    kLognF32Precise = 15,
 };
 
 constexpr bool is_logn_fast(int X) { return X == kLognF32Fast || X == kLognF32FastUnit; }
+constexpr bool is_precise(int X) { return X == kGaussF32Precise || X == kLognF32Precise; }
+// fp32 Box-Muller routes with a shared-memory sin/cos table
+constexpr bool is_f32_table_route(int X) { return X == kGaussF32Fast || is_logn_fast(X) || is_precise(X); }
 
 template <int X> struct XformTraits;
 template <> struct XformTraits<kBits> { using T = uint32_t; static constexpr bool kPair = false; };
@@ -268,6 +279,8 @@ template <> struct XformTraits<kLognF32Accurate> { using T = float; static const
 template <> struct XformTraits<kLognF64> { using T = double; static constexpr bool kPair = true; };
 template <> struct XformTraits<kGaussF32Exact> { using T = float; static constexpr bool kPair = true; };
 template <> struct XformTraits<kGaussF64Exact> { using T = double; static constexpr bool kPair = true; };
+template <> struct XformTraits<kGaussF32Precise> { using T = float; static constexpr bool kPair = true; };
+template <> struct XformTraits<kLognF32Precise> { using T = float; static constexpr bool kPair = true; };
 
 // Single-word transforms.
 template <int X>
@@ -428,13 +441,11 @@ __device__ __forceinline__ double corrected(double approx, int d, const ExactCor
 //    -2 ln 2 multiply: r = sqrt(-lg2(1 - u1)) * sqrt(2 ln 2), and the
 //    sqrt(2 ln 2) is folded into the caller's loop-invariant scale.
 //  * r by MUFU.SQRT (relative error <= 2^-23.2, exhaustive);
-//  * (sin, cos)(2 pi k 2^-24) by angle addition: a per-CTA shared-memory
-//    table of (sin, cos)(2 pi j / 2^TL) (filled by the kernel prologue with
-//    sincospif) for the top TL bits of k, and for the remaining
-//    x < 2 pi 2^-TL: sin x = x, cos x = 1 - x^2/2 (TL < 12) or 1 (TL >= 12:
-//    relative error x^2/2 <= 1.2e-6 on z, inside the 2^-19 tolerance).  x is
-//    built without I2FP or a shift: f = bits(0x3F800000 | (w1 & low-bit
-//    mask)) = 1 + klow 2^-15 (one LOP3), x = (f - 1) 2 pi 2^-9, one FFMA.
+//  * (sin, cos)(2 pi k 2^-24) by angle addition from the NEAREST point of a
+//    per-CTA shared-memory table of (sin, cos)(2 pi j / 2^TL) (kernel
+//    prologue, sincos_tab_entry), residual |x| <= pi 2^-TL: sin x = x,
+//    cos x = 1 - x^2/2 (TL < 12) or 1 (TL >= 12: relative x^2/2 <= 2^-21.7).
+//    See sincos_2pi_k24 (tools/bm_variants.cu measured the variants).
 #ifndef PRNG_BM_TAB_LOG2
 #define PRNG_BM_TAB_LOG2 12
 #endif
@@ -463,25 +474,82 @@ __device__ __forceinline__ float2* sincos_tab() {
 // also folds log2(e), removing the exp's argument multiplies.
 template <int X>
 constexpr bool bm_table_scaled() {
-    return X == kGaussF32Fast || is_logn_fast(X);
+    return is_f32_table_route(X);
 }
 constexpr float kLog2E = 1.4426950408889634f;
 
+// (sin, cos) of the reference's angle fl64(TWO_PI * u2) at table point i of
+// 2^TL (fp32): sincospif's exactly-rounded values, except that the quadrant
+// points carry the reference's non-zero residues cos(fl(pi/2)),
+// sin(fl(pi)), cos(fl(3 pi/2)) (exact zeros would be infinitely many ulps
+// from the reference's tiny outputs there).
+template <int TL>
+__device__ __forceinline__ void sincos_tab_entry(int i, float& sn, float& cs) {
+    sincospif((float)i * (2.0f / (1 << TL)), &sn, &cs);
+    constexpr int Q = 1 << (TL - 2);
+    if ((i & (Q - 1)) == 0) {
+        const int q = i / Q;
+        sn = q == 0 ? 0.0f : q == 1 ? 1.0f : q == 2 ? 1.2246467991473532e-16f : -1.0f;
+        cs = q == 0 ? 1.0f : q == 1 ? 6.123233995736766e-17f : q == 2 ? -1.0f : -1.8369701987210297e-16f;
+    }
+}
+
+// Precise route: -lg2(1 - u1) from a table over the float bits of
+// omx = 1 - u1 (exact): 64 buckets per binade (idx = bits >> 17) for omx in
+// [2^-24, 1].  Entry (inv, lg2(inv)) with inv = the largest fp32 <= 1 / (the
+// bucket's end), so r = 1 - omx inv is in [0, 2^-6] and
+// -lg2(omx) = lg2(inv) - lg2(1 - r) = lg2(inv) + (r + r^2/2 + r^3/3 + r^4/4)/ln 2
+// (truncation r^4/5 < 2^-26 relative): two non-negative terms, so the result
+// keeps its relative accuracy as u1 -> 0 (where lg2.approx's error is
+// absolute).  12 KB next to the 32 KB sin/cos table.
+constexpr int kLogTabIdx0 = 103 << 6;                          // bits(2^-24) >> 17
+constexpr int kLogTabEntries = (127 << 6) - kLogTabIdx0 + 1;  // ... bits(1.0) >> 17
+
+__device__ __forceinline__ float2* log_tab() {
+    __shared__ float2 tab[kLogTabEntries];
+    return tab;
+}
+
 template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform_prologue(const XformParams& p) {
-    if constexpr (X == kGaussF32Fast || is_logn_fast(X)) {
+    if constexpr (is_f32_table_route(X)) {
         float2* tab = sincos_tab<TL>();
         // lognormal: also log2(e), so exp(m + s z) = ex2(fma(rq, cs', m log2(e)))
-        const float S = !bm_table_scaled<X>() ? 1.0f
-                        : is_logn_fast(X)     ? p.scale_f * kBmRq * kLog2E
-                                              : p.scale_f * kBmRq;
+        const float S = !bm_table_scaled<X>()               ? 1.0f
+                        : (is_logn_fast(X) || X == kLognF32Precise) ? p.scale_f * kBmRq * kLog2E
+                                                             : p.scale_f * kBmRq;
         for (int i = threadIdx.x; i < (1 << TL); i += blockDim.x) {
             float sn, cs;
-            sincospif((float)i * (2.0f / (1 << TL)), &sn, &cs);  // angle 2 pi i / 2^TL, exact argument
+            sincos_tab_entry<TL>(i, sn, cs);
             tab[i] = bm_table_scaled<X>() ? make_float2(sn * S, cs * S) : make_float2(sn, cs);
+        }
+        if constexpr (is_precise(X)) {
+            float2* lt = log_tab();
+            for (int i = threadIdx.x; i < kLogTabEntries; i += blockDim.x) {
+                const uint32_t idx = kLogTabIdx0 + i;
+                float inv = 1.0f;
+                if (idx != (127u << 6)) {
+                    inv = __double2float_rd(1.0 / (double)__uint_as_float((idx + 1) << 17));
+                    if (inv < 1.0f) inv = 1.0f;
+                }
+                lt[i] = make_float2(inv, (float)log2((double)inv));
+            }
         }
         __syncthreads();
     }
+}
+
+__device__ __forceinline__ float neg_lg2_1mu_precise(uint32_t w0) {
+    constexpr float c1 = 1.4426950408889634f, c2 = 0.7213475204444817f, c3 = 0.48089834696298783f,
+                    c4 = 0.36067376022224085f;  // 1/(j ln 2)
+    const float kf = __uint2float_rn(w0 >> 8);
+    const float omx = fmaf(kf, -5.9604644775390625e-08f, 1.0f);  // 1 - u1, exact, in [2^-24, 1]
+    const float2 e = log_tab()[(__float_as_uint(omx) >> 17) - kLogTabIdx0];
+    const float r = fmaf(-omx, e.x, 1.0f);
+    float q = fmaf(r, c4, c3);
+    q = fmaf(q, r, c2);
+    q = fmaf(q, r, c1);
+    return fmaf(r, q, e.y);
 }
 
 __device__ __forceinline__ float neg_lg2_1mu(uint32_t w0) {
@@ -508,22 +576,31 @@ __device__ __forceinline__ float neg_lg2_1mu(uint32_t w0) {
     }
 }
 
-template <int TL>
+// sin/cos(2 pi k 2^-24), k = w1 >> 8, by angle addition from the table
+// point NEAREST to the angle (round-to-nearest index: (w1 + half a bucket)
+// >> (32 - TL), wrapping to 0 at 2 pi): the quadrant points are table points,
+// so results near the zeros of sin/cos keep their relative accuracy, and the
+// residual angle |x| <= pi 2^-TL is half the truncated form's.  x is built
+// without I2FP or a shift: the L = 24 - TL low bits of k stay in place as
+// mantissa bits [8, 8 + L) under 1.0f (one LOP3), f - (1 + 2^(L-1) 2^-15)
+// is the signed offset from the bucket centre times 2^-15 (exact), times
+// 2 pi 2^-9.  sin x = x and cos x = 1 for TL >= 12 (|x| <= 7.7e-4:
+// relative x^2/2 <= 2^-21.7), cos x = 1 - x^2/2 below.
+template <int TL, bool QUAD = (TL < PRNG_BM_COS_QUAD_BELOW)>
 __device__ __forceinline__ void sincos_2pi_k24(uint32_t w1, float& sn, float& cs) {
-    constexpr int L = 24 - TL;  // low bits of k = w1 >> 8 left to the polynomial
+    constexpr int L = 24 - TL;  // low bits of k left to the polynomial
     static_assert(L >= 1 && L <= 15, "table size");
-    const float2 t = sincos_tab<TL>()[w1 >> (32 - TL)];
-    // bits [8, 8 + L) of w1 stay where they are, as mantissa bits [8, 8 + L)
-    // under the exponent of 1.0f (one LOP3, no shift): f - 1 = low * 2^-15.
-    uint32_t fb;  // (w1 & mask) | bits(1.0f) as ONE 3-input LOP3 (one operand in a register)
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(fb) : "r"(w1), "n"(((1u << L) - 1u) << 8), "r"(0x3F800000u));
-    const float f = __uint_as_float(fb);
-    constexpr float C = 3.7450702e-07f * 32768.0f;  // 2 pi 2^-9 (power-of-two scaling of 2 pi 2^-24)
-    const float x = fmaf(f, C, -C);
-    if constexpr (TL < PRNG_BM_COS_QUAD_BELOW) {
-        const float cl = fmaf(x * x, -0.5f, 1.0f);
-        sn = fmaf(t.y, x, t.x * cl);
-        cs = fmaf(-t.x, x, t.y * cl);
+    const uint32_t wc = w1 + (1u << (31 - TL));
+    const float2 t = sincos_tab<TL>()[wc >> (32 - TL)];
+    uint32_t fb;  // (wc & mask) | bits(1.0f) as ONE 3-input LOP3 (one operand in a register)
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(fb) : "r"(wc), "n"(((1u << L) - 1u) << 8), "r"(0x3F800000u));
+    constexpr float kCentre = 1.0f + (float)(1u << (L - 1)) * 3.0517578125e-05f;  // 1 + 2^(L-1) 2^-15
+    const float d = __fsub_rn(__uint_as_float(fb), kCentre);                         // exact
+    const float x = __fmul_rn(d, 0.01227184630308513f);                              // 2 pi 2^-9
+    if constexpr (QUAD) {
+        const float nh = __fmul_rn(x, __fmul_rn(x, -0.5f));
+        sn = fmaf(t.y, x, fmaf(t.x, nh, t.x));
+        cs = fmaf(-t.x, x, fmaf(t.y, nh, t.y));
     } else {
         sn = fmaf(t.y, x, t.x);
         cs = fmaf(-t.x, x, t.y);
@@ -536,6 +613,15 @@ __device__ __forceinline__ void box_muller_f32_parts(uint32_t w0, uint32_t w1, f
     const float s = neg_lg2_1mu(w0);
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(s));  // s = 0 or >= 1.7e-7
     sincos_2pi_k24<TL>(w1, sn, cs);
+}
+
+// Precise route: table log, sqrt.approx, centred sin/cos with the x^2 term.
+template <int TL>
+__device__ __forceinline__ void box_muller_f32_parts_precise(uint32_t w0, uint32_t w1, float& rq, float& sn,
+                                                             float& cs) {
+    const float s = neg_lg2_1mu_precise(w0);
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rq) : "f"(s));
+    sincos_2pi_k24<TL, true>(w1, sn, cs);
 }
 
 template <int X>
@@ -595,12 +681,47 @@ template <> __device__ __forceinline__ void xform2<kGaussF64Exact>(uint32_t w0, 
     o1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
 }
 
+// fp32 exact route (Ziv's rounding test).  The reference's fp32 output is
+// RN32(v), v = fl(fl(z sd) + mean), z its fp64 Box-Muller value.  The
+// uncorrected device value v' differs from v by at most
+//   tol = sd (|z'| (rel_log / 2 + 4 u) + r' abs_sc) + 2 u (sd |z'| + |v'|),  u = 2^-53
+// (sqrt and the products rounded on both sides; rel_log / abs_sc measured
+// over the whole domains when the tables are built), doubled for margin.
+// RN32(v') == RN32(v) unless v' lies within tol of an fp32 rounding
+// boundary (the midpoint between the two fp32 values around it); only then
+// -- about 2^-20 of the pairs -- are the correction tables read.  No random
+// gathers on the common path, so the route runs at the fp64 formula's speed.
+__device__ __forceinline__ bool f32_rounding_uncertain(double v, double tol) {
+    const float f = __double2float_rn(v);
+    const double fd = (double)f;
+    const float g = nextafterf(f, v > fd ? INFINITY : -INFINITY);
+    const double mid = 0.5 * (fd + (double)g);  // exact: two fp32 values
+    return fabs(v - mid) <= tol;
+}
+
 template <> __device__ __forceinline__ void xform2<kGaussF32Exact>(uint32_t w0, uint32_t w1, const XformParams& p,
                                                                   float& o0, float& o1) {
-    double a, b;
-    xform2<kGaussF64Exact>(w0, w1, p, a, b);
-    o0 = (float)a;  // .astype(float32) (distributions.py:131)
-    o1 = (float)b;
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log_u1_f64(w0)));
+    double s, c;
+    sincos_ref_f64(w1, s, c);
+    const double z0 = __dmul_rn(r, c), z1 = __dmul_rn(r, s);
+    const double v0 = __dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);
+    const double v1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
+    constexpr double u = 1.1102230246251565e-16;  // 2^-53
+    const double rz = 0.5 * p.exact.rel_log + 4.0 * u;
+    const double rb = r * p.exact.abs_sc;
+    const double sd = p.scale_d;
+    const double t0 = 2.0 * (sd * (fabs(z0) * rz + rb) + 2.0 * u * (sd * fabs(z0) + fabs(v0)));
+    const double t1 = 2.0 * (sd * (fabs(z1) * rz + rb) + 2.0 * u * (sd * fabs(z1) + fabs(v1)));
+    if (f32_rounding_uncertain(v0, t0) || f32_rounding_uncertain(v1, t1)) {
+        double a, b;
+        xform2<kGaussF64Exact>(w0, w1, p, a, b);
+        o0 = (float)a;  // .astype(float32) (distributions.py:131)
+        o1 = (float)b;
+        return;
+    }
+    o0 = (float)v0;
+    o1 = (float)v1;
 }
 
 // Lognormal (extension a18): x = exp(m + s*z) * scale + displ.
@@ -628,12 +749,15 @@ template <> __device__ __forceinline__ void xform2<kLognF32Accurate>(uint32_t w0
 template <int X, int TL = kPhiloxTabLog2>
 __device__ __forceinline__ void xform2k(uint32_t w0, uint32_t w1, const XformParams& p,
                                         typename XformTraits<X>::T& o0, typename XformTraits<X>::T& o1) {
-    if constexpr (X == kGaussF32Fast || is_logn_fast(X)) {
+    if constexpr (is_f32_table_route(X)) {
         float rq, sn, cs;
-        box_muller_f32_parts<TL>(w0, w1, rq, sn, cs);
+        if constexpr (is_precise(X))
+            box_muller_f32_parts_precise<TL>(w0, w1, rq, sn, cs);
+        else
+            box_muller_f32_parts<TL>(w0, w1, rq, sn, cs);
         // stddev and sqrt(2 ln 2) folded into r (loop-invariant) or into the table
         const float rs = bm_table_scaled<X>() ? rq : rq * (p.scale_f * kBmRq);
-        if constexpr (X == kGaussF32Fast) {
+        if constexpr (X == kGaussF32Fast || X == kGaussF32Precise) {
             o0 = fmaf(rs, cs, p.off_f);
             o1 = fmaf(rs, sn, p.off_f);
         } else {

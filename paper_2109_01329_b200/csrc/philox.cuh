@@ -118,11 +118,16 @@ constexpr bool philox_rk() {
 #ifndef PRNG_PHILOX_PIPE
 #define PRNG_PHILOX_PIPE 1
 #endif
+#ifndef PRNG_GAUSS_MINB  // min resident CTAs for the unpipelined fast Box-Muller kernels
+#define PRNG_GAUSS_MINB 0
+#endif
 // Aligned-path software pipelining (Philox of pass i+1 next to the transform
-// of pass i) for the fast fp32 Box-Muller transforms.
+// of pass i): the fast fp32 lognormal (+3% in-library, 4-CTA bound); the
+// centred-table fast gaussian is 1.8% faster unpipelined with no bound
+// (tools/ab_lib.py, gpurun_out r2_9).
 template <int X>
 constexpr bool philox_pipelined() {
-    return PRNG_PHILOX_PIPE && (X == kGaussF32Fast || is_logn_fast(X));
+    return PRNG_PHILOX_PIPE && is_logn_fast(X);
 }
 template <> struct PhiloxBpt<double> { static constexpr int kValue = 2; };
 
@@ -298,8 +303,9 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
 template <int X, int SHIFT>
 constexpr int philox_min_blocks() {
     return (X == kUnitF32 || X == kUniformF32) ? (SHIFT == 0 ? PRNG_UNIT_MINB : 4)
-           : (X == kGaussF32Fast && philox_pipelined<X>() && SHIFT == 0) ? 4
-                                                                          : 0;
+           : ((X == kGaussF32Fast || is_logn_fast(X)) && SHIFT == 0) ? (philox_pipelined<X>() ? 4 : PRNG_GAUSS_MINB)
+           : (is_precise(X) && SHIFT == 0) ? 5  // 45 KB of tables: at most 5 CTAs per SM
+                                           : 0;
 }
 
 template <int X, int SHIFT>

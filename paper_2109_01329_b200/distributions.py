@@ -15,8 +15,11 @@ Results vs the reference:
   * gaussian/lognormal fp64, and fp32 with method="accurate": fp64 math on
     the device (CUDA libdevice log/sincos/exp vs glibc), a few fp64 ulps;
   * gaussian/lognormal fp32 with method="fast" (default): fp32 SFU lg2 /
-    sqrt (series near u1 = 0), table-driven sin/cos, ex2, within the stated
-    fp32 tolerance;
+    sqrt (series near u1 = 0), sin/cos from the nearest point of a table,
+    ex2: |err| <= 2^-20 * stddev * max(1, |z|), <= 8 ulp for |z| >= 1;
+  * method="precise" (fp32): table log + centred sin/cos with the x^2 term,
+    within 5 ulp of the reference for every input (lognormal: 5 ulp *
+    max(1, |ln x|)), ~85% of "fast"'s throughput;
   * gaussian fp32/fp64 with method="exact": bit-identical to the reference
     (device log / sin / cos corrected to the host libm by per-input ulp
     deltas over their whole 2^24-point input domains, csrc/common.cuh
@@ -50,7 +53,8 @@ from .errors import InvalidParameter, InvalidRange, UnsupportedEngine
 
 _UNIT_SCALE = 2.0 ** -24
 _PRECISIONS = ("fp32", "fp64")
-_METHODS = {"fast": _lib.METHOD_FAST, "accurate": _lib.METHOD_ACCURATE, "exact": _lib.METHOD_EXACT}
+_METHODS = {"fast": _lib.METHOD_FAST, "accurate": _lib.METHOD_ACCURATE, "exact": _lib.METHOD_EXACT,
+            "precise": _lib.METHOD_PRECISE}
 
 
 def _check_precision(precision: str) -> None:
@@ -60,7 +64,7 @@ def _check_precision(precision: str) -> None:
 
 def _check_method(method: str, exact_ok: bool = True) -> None:
     if method not in _METHODS or (method == "exact" and not exact_ok):
-        allowed = "'fast', 'accurate' or 'exact'" if exact_ok else "'fast' or 'accurate'"
+        allowed = "'fast', 'precise', 'accurate' or 'exact'" if exact_ok else "'fast', 'precise' or 'accurate'"
         raise InvalidParameter(f"method must be {allowed}, got {method!r}")
 
 

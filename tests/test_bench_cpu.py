@@ -25,12 +25,13 @@ def _slice(workload, n, rank):
     return O.generate(engine, st, dist, n, prec, a, b)
 
 
-@pytest.mark.parametrize("workload", ["c1", "c4", "c4_bits", "c2", "c3_gauss", "c3_logn"])
+@pytest.mark.parametrize("workload", ["c1", "c4", "c4_bits", "c2", "c3_gauss", "c3_logn", "c3_gauss_precise",
+                                      "c3_logn_precise", "c3_gauss_exact"])
 @pytest.mark.parametrize("rank", [0, 3])
 def test_slice_check_accepts_oracle_slices(workload, rank):
     n = 1 << 14
     engine, dist, prec, _, _ = bench.WORKLOADS[workload]
-    spec = bench.make_spec(P, dist, prec)
+    spec = bench.make_spec(P, dist, prec, bench.WORKLOAD_METHOD.get(workload, "fast"))
     want = _slice(workload, n, rank)
     ok, worst = bench.slice_check(P, torch, workload, spec, torch.from_numpy(want.copy()), n, rank)
     assert ok and worst <= 1.0

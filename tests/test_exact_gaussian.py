@@ -79,3 +79,28 @@ def test_exact_gaussian_matches_reference_golden(golden, golden_arrays):
         a = P.gaussian_from_words(words, 0.25, 2.0, 4095, prec, method="exact").cpu().numpy()
         b = O.gaussian_from_words(words.cpu().numpy(), 0.25, 2.0, 4095, prec)
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+def test_exact_route_rounding_test_bounds_and_cancellation_cases():
+    """The fp32 exact route skips the correction tables unless the fp64
+    value sits within its error bound of an fp32 rounding boundary.  The
+    bounds it uses are the worst approximation errors measured over the
+    whole domains; they must be tiny (a few fp64 ulps).  Outputs stay
+    bit-identical where the affine cancels (mean ~ -z * sd), the case the
+    bound's |v| terms exist for."""
+    import ctypes
+    import json
+
+    b = (ctypes.c_double * 2)()
+    esc = ctypes.c_uint64()
+    P._lib.check(P._lib.lib.prng_exact_tables_bounds(b, ctypes.byref(esc)))
+    print(json.dumps({"exact_bounds": {"rel_log": b[0], "abs_sincos": b[1], "escapes": esc.value}}))
+    assert 0 <= b[0] < 2.0 ** -48 and 0 <= b[1] < 2.0 ** -50
+    st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 2024)
+    for mean, sd in ((-1.0, 1.0), (1.0, 1.0), (1e-3, 1e-3), (-3.0, 1.0), (0.0, 1e-30), (1e20, 1e20)):
+        n = 1 << 20
+        _, got = P.generate(P.Gaussian(mean, sd, "fp32", "exact"), st, n)
+        want = O.generate("philox", (O.seed_philox(2024), 0), "gaussian", n, "fp32", mean, sd)
+        assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), (mean, sd)
