@@ -53,6 +53,8 @@ WORKLOADS = {
                          "philox4x32x10 seed=777 gaussian fp32 (0,1) method=precise (C3)"),
     "c3_logn_precise": ("philox", "lognormal", "fp32", 1 << 30,
                         "philox4x32x10 seed=777 lognormal fp32 (0,1) method=precise (C3)"),
+    "c3_gauss_accurate": ("philox", "gaussian", "fp32", 1 << 30,
+                          "philox4x32x10 seed=777 gaussian fp32 (0,1) method=accurate (C3, fp64 math)"),
     "c3_gauss_exact": ("philox", "gaussian", "fp32", 1 << 30,
                        "philox4x32x10 seed=777 gaussian fp32 (0,1) method=exact (C3, bit-exact)"),
     "c5": ("philox", "uniform", "fp32", 0, "FastCaloSim-style ~10^4 x 200k fp32 batches (C5)"),
@@ -69,8 +71,10 @@ KERNEL_NAMES = {
     "c3_gauss_precise": "philox_kernel<kGaussF32Precise, SHIFT=0>",
     "c3_logn_precise": "philox_kernel<kLognF32Precise, SHIFT=0>",
     "c3_gauss_exact": "philox_kernel<kGaussF32Exact, SHIFT=0>",
+    "c3_gauss_accurate": "philox_kernel<kGaussF32Accurate, SHIFT=0>",
 }
 WORKLOAD_METHOD = {"c3_gauss_precise": "precise", "c3_logn_precise": "precise", "c3_gauss_exact": "exact",
+                   "c3_gauss_accurate": "accurate",
 }
 
 
@@ -451,6 +455,54 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+PLUGIN_E2E_CHILD = r"""
+import json, os, sys, time
+import portarng._kernels as K
+from portarng import distributions, engine, execution, rngburn
+assert K.IMPL == os.environ["PORTARNG_KERNELS"], K.IMPL
+n, ncpu = int(sys.argv[1]), os.cpu_count() or 1
+os.environ[execution.ARENA_ENV_VAR] = str(max(2 * 1024 ** 3, 8 * n))
+spec = distributions.Uniform(0.0, 1.0, "fp32")
+res = {}
+for mode, backend in (("buffer", execution.Parallel(workers=ncpu)), ("hostdirect", execution.Serial())):
+    ts = []
+    for _ in range(4):
+        tts, host = rngburn.burn_once(engine.EngineKind.PHILOX4X32X10, spec, mode, backend, n, 777)
+        ts.append(tts / 1e9)
+    assert abs(float(host[0]) - 0.35297131538391113) < 1e-12 and len(host) == n
+    res[mode] = n / min(ts[1:]) / 1e9
+print(json.dumps(res))
+"""
+
+
+def plugin_e2e(n):
+    """The reference's own public path with its kernel seam bound to the B200
+    (INTEGRATION.md §1 stub, PORTARNG_KERNELS=cuda): stock
+    rngburn.burn_once(PHILOX4X32X10, Uniform(0, 1, fp32), "buffer",
+    Parallel(os.cpu_count()) / "hostdirect", Serial, n, 777) -- words from
+    the GPU through prng_kernels_philox_fill (pinned, double-buffered D2H),
+    the reference's numpy unit/affine passes on the host.  Also the same
+    cycle with the stock compiled core for the ratio.  Subprocesses, so the
+    selector sees a fresh import."""
+    import subprocess
+
+    if not (STAGED_REF / "src" / "portarng" / "_kernels" / "_cuda.py").exists():
+        return None
+    out = {"n_per_cycle": n, "metric": "Gsamples/s (TTS of one burn_once cycle, best of 3 after one warm-up)"}
+    for impl in ("cuda", "core"):
+        env = dict(os.environ, PORTARNG_KERNELS=impl, PYTHONPATH=str(STAGED_REF / "src"),
+                   PRNG_B200_LIB=str(ROOT / "paper_2109_01329_b200" / "libprng_b200.so"))
+        r = subprocess.run([sys.executable, "-c", PLUGIN_E2E_CHILD, str(n)], env=env, capture_output=True, text=True,
+                           timeout=900)
+        if r.returncode:
+            log(f"plugin e2e ({impl}) failed: {r.stderr[-600:]}")
+            return None
+        out[impl] = json.loads(r.stdout.strip().splitlines()[-1])
+    out["source"] = ("stock portarng rngburn.burn_once from baseline/_ref, _kernels seam bound to "
+                     "libprng_b200.so (cuda) vs the compiled Cython core (core)")
+    return out
 
 
 def graph_time_per_launch(torch, fn, k=20, reps=5):
@@ -861,6 +913,9 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.workload in ("c1", "c2", "c3_gauss", "c4"):
         cpu = cpu_baseline_sample(args.cpu_n, args.workload)
+    seam = None
+    if rank == 0 and world == 1 and args.workload == "c4" and not args.no_e2e and not args.no_plugin_e2e:
+        seam = plugin_e2e(args.plugin_n)
 
     sweep = None
     if args.sweep:
@@ -915,6 +970,7 @@ def run_ours(args):
             "ranks": ranks_info,
             "backend": backend,
             "e2e": e2e,
+            "e2e_reference_seam": seam,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
@@ -949,6 +1005,8 @@ def main():
     ap.add_argument("--sustained", type=int, default=150,
                     help="back-to-back launches after the timed region for the sustained number (0 = off)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-plugin-e2e", action="store_true", help="skip burn_once through the CUDA plugin seam")
+    ap.add_argument("--plugin-n", type=int, default=1 << 28, help="samples per burn_once cycle for the seam e2e")
     ap.add_argument("--out-offset", type=int, default=0, help="output view offset in elements (odd: misaligned pairs)")
     ap.add_argument("--sweep", action="store_true", help="also run the C4 batch-size sweep (CUDA-graph timed)")
     ap.add_argument("--sweep-max", type=int, default=32)

@@ -151,10 +151,10 @@ int prng_gaussian_from_words_f64_method(const uint32_t *words, uint64_t n, doubl
 int prng_exact_tables_prepare(void);
 int prng_exact_tables_host(const double **log_table, const double **sincos_table);
 /* The current device's exact tables (built if needed): worst relative error
- * of the device log approximation and worst absolute error of its sin/cos
- * against the host libm over the whole domains (bounds[0], bounds[1]) --
- * the fp32 exact route's rounding test uses them -- and the number of
- * escape-list entries. */
+ * of the short device log approximation and worst absolute error of its
+ * sin/cos against the host libm over both whole domains (bounds[0],
+ * bounds[1]) -- the fp32 exact route's rounding test uses them -- and the
+ * number of escape-list entries of the corrections. */
 int prng_exact_tables_bounds(double bounds[2], uint64_t *escapes);
 
 /* ---- Many small batches (FastCaloSim consumer, calosim.py:269-358). ----

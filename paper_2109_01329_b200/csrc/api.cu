@@ -204,6 +204,29 @@ __global__ void exact_approx_kernel(double* L, double* S, double* C) {
     }
 }
 
+// Worst differences of the short approximations (the fp32 exact route's
+// common path) from the full ones over both whole domains: [0] relative for
+// the log, [1] absolute for sin / cos (non-negative doubles order like their
+// bit patterns, so atomicMax on the bits).
+__global__ void exact_short_bounds_kernel(unsigned long long* out) {
+    double rl = 0.0, asc = 0.0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < (uint32_t)kExactN; i += gridDim.x * blockDim.x) {
+        const uint32_t w0 = (16777215u - i) << 8;
+        const double a = log_u1_f64(w0), b = log_u1_f64_short(w0);
+        if (a != 0.0) rl = fmax(rl, fabs(b - a) / fabs(a));
+        else if (b != 0.0) rl = INFINITY;
+        double s, c, s2, c2;
+        sincos_2pi_k24_f64(i, s, c);
+        sincos_f64_short(i << 8, s2, c2);
+        double s3, c3;
+        sincos_ref_f64(i << 8, s3, c3);  // the full form incl. the argument-rounding term
+        asc = fmax(asc, fmax(fabs(s2 - s3), fabs(c2 - c3)));
+        (void)s; (void)c;
+    }
+    atomicMax(out, (unsigned long long)__double_as_longlong(rl));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(asc));
+}
+
 struct ExactDevice {
     ExactCorrections corr{};
     size_t escapes = 0;
@@ -264,8 +287,26 @@ int exact_tables_build(ExactDevice& ed, cudaStream_t st) {
         }
         abs_sc = std::max(abs_sc, std::max(std::fabs(aS[i] - g_exact_sc[i].x), std::fabs(aC[i] - g_exact_sc[i].y)));
     }
-    ed.corr.rel_log = rel_log;
-    ed.corr.abs_sc = abs_sc;
+    // the short forms' bounds: |short - libm| <= |short - full| + |full - libm|
+    unsigned long long* dmax = nullptr;
+    PRNG_CUDA(cudaMallocAsync((void**)&dmax, 2 * sizeof(unsigned long long), st));
+    PRNG_CUDA(cudaMemsetAsync(dmax, 0, 2 * sizeof(unsigned long long), st));
+    exact_short_bounds_kernel<<<1184, 256, 0, st>>>(dmax);
+    unsigned long long hmax[2] = {0, 0};
+    PRNG_CUDA(cudaGetLastError());
+    PRNG_CUDA(cudaMemcpyAsync(hmax, dmax, sizeof hmax, cudaMemcpyDeviceToHost, st));
+    PRNG_CUDA(cudaFreeAsync(dmax, st));
+    PRNG_CUDA(cudaStreamSynchronize(st));
+    double rs, as;
+    memcpy(&rs, &hmax[0], 8);
+    memcpy(&as, &hmax[1], 8);
+    const double rel_short = rs * (1.0 + rel_log) + rel_log;
+    const double abs_short = as + abs_sc;
+    ed.corr.rel_log = rel_short;
+    ed.corr.abs_sc = abs_short;
+    ed.corr.tol_c = std::isfinite(rel_short)
+                        ? nextafterf((float)(2.0 * (0.5 * rel_short + abs_short + 6.0 * 0x1p-53)), INFINITY)
+                        : INFINITY;
     std::vector<uint32_t> eidx[3];
     std::vector<double> eval[3];
     for (size_t i = 0; i < kExactN; ++i) {
@@ -450,6 +491,13 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
                        : shift == 1 ? (const void*)philox_kernel<X, 1>
                        : shift == 2 ? (const void*)philox_kernel<X, 2>
                                     : (const void*)philox_kernel<X, 3>;
+    if constexpr (kPair) {
+        if (mis)
+            kern = shift == 0   ? (const void*)philox_kernel<X, 0, true>
+                   : shift == 1 ? (const void*)philox_kernel<X, 1, true>
+                   : shift == 2 ? (const void*)philox_kernel<X, 2, true>
+                                : (const void*)philox_kernel<X, 3, true>;
+    }
     int sms = 0, occ = 0;
     rc = resident_ctas(kern, kPhiloxThreads, &sms, &occ);
     if (rc) return rc;

@@ -219,12 +219,13 @@ struct ExactCorrections {
     const uint32_t* esc_idx[3];  // escapes (correction -8): sorted indices ...
     const double* esc_val[3];    // ... and the host-libm values; [0] log, [1] sin, [2] cos
     uint32_t esc_n[3];
-    // Worst differences of the approximations from the host libm over the
-    // whole domains (measured when the tables are built): relative for
-    // log_u1_f64, absolute for sincos_ref_f64.  The fp32 exact route uses
-    // them to decide when the uncorrected value already rounds like the
-    // reference's (box_muller_f32_exact).
+    // Worst differences of the short approximations (log_u1_f64_short,
+    // sincos_f64_short) from the host libm over both whole domains (measured
+    // when the tables are built): relative for the log, absolute for sin /
+    // cos.  The fp32 exact route's rounding test (f32_rounding_uncertain)
+    // uses them.
     double rel_log, abs_sc;
+    float tol_c;  // 2 (rel_log / 2 + abs_sc + 6 * 2^-53), rounded up (f32_rounding_uncertain)
 };
 
 // Parameters of one fused request.  For uniform: (a, b) -> scale/offset with
@@ -339,7 +340,8 @@ __constant__ double kCosC[10] = {1.0,                    -0.30842513753404244,  
 // log(u1'), u1' = 1 - (w0 >> 8) 2^-24 = m 2^-24 (intrinsics only: no
 // contraction freedom, so the exact method's correction tables, built by
 // running this same code, stay valid).
-__device__ __forceinline__ double log_u1_f64(uint32_t w0) {
+template <int TERMS = 9>
+__device__ __forceinline__ double log_u1_f64_t(uint32_t w0) {
     const double x = __uint2double_rn(16777216u - (w0 >> 8));  // m, exact, in [1, 2^24]
     const int hi = __double2hiint(x);
     const int e = (hi - 0x3FE6A09E) >> 20;  // 0x3FE6A09E: high word of sqrt(1/2)
@@ -354,27 +356,28 @@ __device__ __forceinline__ double log_u1_f64(uint32_t w0) {
     rd = __fma_rn(rd, er, rd);
     const double s = __dmul_rn(g, rd);
     const double z = __dmul_rn(s, s);
-    double p = kAtanhC[8];
+    double p = kAtanhC[TERMS - 1];
 #pragma unroll
-    for (int i = 7; i >= 0; --i) p = __fma_rn(p, z, kAtanhC[i]);
+    for (int i = TERMS - 2; i >= 0; --i) p = __fma_rn(p, z, kAtanhC[i]);
     const double s2 = __dmul_rn(2.0, s);
     const double lnf = __fma_rn(s2, __dmul_rn(z, p), s2);
     const double ee = (double)(e - 24);
     return __fma_rn(ee, kLn2Split[0], __fma_rn(ee, kLn2Split[1], lnf));
 }
 
-__device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, double& cs) {
+template <int SIN_TERMS = 9, int COS_TERMS = 10>
+__device__ __forceinline__ void sincos_2pi_k24_f64_t(uint32_t k, double& sn, double& cs) {
     const uint32_t kk = k + (1u << 21);
     const uint32_t q = (kk >> 22) & 3u;
     const double t = __dmul_rn((double)((int)(kk & 0x3FFFFFu) - (1 << 21)), 4.76837158203125e-07);  // exact
     const double t2 = __dmul_rn(t, t);
-    double s = kSinC[8];
+    double s = kSinC[SIN_TERMS - 1];
 #pragma unroll
-    for (int i = 7; i >= 0; --i) s = __fma_rn(s, t2, kSinC[i]);
+    for (int i = SIN_TERMS - 2; i >= 0; --i) s = __fma_rn(s, t2, kSinC[i]);
     s = __dmul_rn(s, t);
-    double c = kCosC[9];
+    double c = kCosC[COS_TERMS - 1];
 #pragma unroll
-    for (int i = 8; i >= 0; --i) c = __fma_rn(c, t2, kCosC[i]);
+    for (int i = COS_TERMS - 2; i >= 0; --i) c = __fma_rn(c, t2, kCosC[i]);
     const bool swap = q & 1u;
     const double a = swap ? s : c;
     const double b = swap ? c : s;
@@ -388,6 +391,23 @@ __device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, doubl
 // a first-order correction on the exactly reduced 2 pi k 2^-24 reproduces it
 // (and the reference's non-zero values at the quadrant points, e.g.
 // cos(fl(pi/2))).
+__device__ __forceinline__ double log_u1_f64(uint32_t w0) { return log_u1_f64_t<9>(w0); }
+__device__ __forceinline__ void sincos_2pi_k24_f64(uint32_t k, double& sn, double& cs) {
+    sincos_2pi_k24_f64_t<9, 10>(k, sn, cs);
+}
+
+// Shorter forms for the fp32 exact route's common path (~2^-44 instead of a
+// few ulps; no first-order argument-rounding term): its rounding test only
+// needs an error BOUND, which the table build measures over both whole
+// domains (exact_fast_bounds_kernel).
+#ifndef PRNG_EXACT_SHORT
+#define PRNG_EXACT_SHORT 1
+#endif
+__device__ __forceinline__ double log_u1_f64_short(uint32_t w0) { return log_u1_f64_t<PRNG_EXACT_SHORT ? 7 : 9>(w0); }
+__device__ __forceinline__ void sincos_f64_short(uint32_t w1, double& sn, double& cs) {
+    sincos_2pi_k24_f64_t<PRNG_EXACT_SHORT ? 7 : 9, PRNG_EXACT_SHORT ? 8 : 10>(w1 >> 8, sn, cs);
+}
+
 __device__ __forceinline__ void sincos_ref_f64(uint32_t w1, double& sn, double& cs) {
     double s, c;
     sincos_2pi_k24_f64(w1 >> 8, s, c);
@@ -683,45 +703,68 @@ template <> __device__ __forceinline__ void xform2<kGaussF64Exact>(uint32_t w0, 
 
 // fp32 exact route (Ziv's rounding test).  The reference's fp32 output is
 // RN32(v), v = fl(fl(z sd) + mean), z its fp64 Box-Muller value.  The
-// uncorrected device value v' differs from v by at most
-//   tol = sd (|z'| (rel_log / 2 + 4 u) + r' abs_sc) + 2 u (sd |z'| + |v'|),  u = 2^-53
-// (sqrt and the products rounded on both sides; rel_log / abs_sc measured
-// over the whole domains when the tables are built), doubled for margin.
-// RN32(v') == RN32(v) unless v' lies within tol of an fp32 rounding
-// boundary (the midpoint between the two fp32 values around it); only then
-// -- about 2^-20 of the pairs -- are the correction tables read.  No random
-// gathers on the common path, so the route runs at the fp64 formula's speed.
-__device__ __forceinline__ bool f32_rounding_uncertain(double v, double tol) {
-    const float f = __double2float_rn(v);
-    const double fd = (double)f;
-    const float g = nextafterf(f, v > fd ? INFINITY : -INFINITY);
-    const double mid = 0.5 * (fd + (double)g);  // exact: two fp32 values
-    return fabs(v - mid) <= tol;
+// uncorrected device value v' (the short fp64 approximations) differs from
+// v by at most
+//   sd (|z'| (rel_log / 2 + 4 u) + r' abs_sc) + 2 u (sd |z'| + |v'|)
+//   <= C (sd r' + |v'|),   C = rel_log / 2 + abs_sc + 6 u,  u = 2^-53
+// (sqrt and the products rounded on both sides, |z'| <= r'; rel_log and
+// abs_sc measured over the whole domains when the tables are built); the
+// test uses twice that, evaluated in fp32.  RN32(v') == RN32(v) unless v'
+// lies within it of an fp32 rounding boundary -- i.e. unless the 29 mantissa
+// bits fp32 drops are within tol / ulp64(v') of 2^28 -- and only then
+// (~2^-20 of the pairs, plus |v'| outside [2^-74, 2^127)) are the correction
+// tables read.  The test is integer / fp32 work; the FP64 pipe does only the
+// accurate route's formula.
+__device__ __forceinline__ bool f32_rounding_uncertain(double v, float tol) {
+    const uint32_t lo = (uint32_t)__double2loint(v);
+    const uint32_t e = ((uint32_t)__double2hiint(v) >> 20) & 0x7FFu;  // biased fp64 exponent
+    if (e < 949u || e > 1149u) return true;  // |v| < 2^-74 or >= 2^127
+    const int d = abs((int)(lo & 0x1FFFFFFFu) - (1 << 28));  // ulp64s to the boundary
+    const float ulp = __uint_as_float((e - 948u) << 23);     // 2^(e - 1075) = ulp64(v)
+    return (float)d * ulp <= tol;
+}
+
+// The corrected pair (rare path of the fp32 exact route), out of line so the
+// common path keeps its registers.
+#ifndef PRNG_EXACT_NOINLINE
+#define PRNG_EXACT_NOINLINE 0
+#endif
+#if PRNG_EXACT_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+void exact_pair_f32(uint32_t w0, uint32_t w1, double sd, double mean, const ExactCorrections x, float& o0,
+                    float& o1) {
+    XformParams q{};
+    q.scale_d = sd;
+    q.off_d = mean;
+    q.exact = x;
+    double a, b;
+    box_muller_exact(w0, w1, q, a, b);
+    o0 = (float)__dadd_rn(__dmul_rn(a, sd), mean);
+    o1 = (float)__dadd_rn(__dmul_rn(b, sd), mean);
+}
+
+// The common path of the fp32 exact route: the uncorrected pair and whether
+// either output's rounding is uncertain (then exact_pair_f32 decides).
+__device__ __forceinline__ bool gauss_f32_exact_try(uint32_t w0, uint32_t w1, const XformParams& p, float& o0,
+                                                    float& o1) {
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log_u1_f64_short(w0)));
+    double s, c;
+    sincos_f64_short(w1, s, c);
+    const double v0 = __dadd_rn(__dmul_rn(__dmul_rn(r, c), p.scale_d), p.off_d);
+    const double v1 = __dadd_rn(__dmul_rn(__dmul_rn(r, s), p.scale_d), p.off_d);
+    o0 = (float)v0;  // .astype(float32) (distributions.py:131)
+    o1 = (float)v1;
+    const float base = p.exact.tol_c * p.scale_f * (float)r;
+    return f32_rounding_uncertain(v0, fmaf(p.exact.tol_c, fabsf(o0), base)) ||
+           f32_rounding_uncertain(v1, fmaf(p.exact.tol_c, fabsf(o1), base));
 }
 
 template <> __device__ __forceinline__ void xform2<kGaussF32Exact>(uint32_t w0, uint32_t w1, const XformParams& p,
                                                                   float& o0, float& o1) {
-    const double r = __dsqrt_rn(__dmul_rn(-2.0, log_u1_f64(w0)));
-    double s, c;
-    sincos_ref_f64(w1, s, c);
-    const double z0 = __dmul_rn(r, c), z1 = __dmul_rn(r, s);
-    const double v0 = __dadd_rn(__dmul_rn(z0, p.scale_d), p.off_d);
-    const double v1 = __dadd_rn(__dmul_rn(z1, p.scale_d), p.off_d);
-    constexpr double u = 1.1102230246251565e-16;  // 2^-53
-    const double rz = 0.5 * p.exact.rel_log + 4.0 * u;
-    const double rb = r * p.exact.abs_sc;
-    const double sd = p.scale_d;
-    const double t0 = 2.0 * (sd * (fabs(z0) * rz + rb) + 2.0 * u * (sd * fabs(z0) + fabs(v0)));
-    const double t1 = 2.0 * (sd * (fabs(z1) * rz + rb) + 2.0 * u * (sd * fabs(z1) + fabs(v1)));
-    if (f32_rounding_uncertain(v0, t0) || f32_rounding_uncertain(v1, t1)) {
-        double a, b;
-        xform2<kGaussF64Exact>(w0, w1, p, a, b);
-        o0 = (float)a;  // .astype(float32) (distributions.py:131)
-        o1 = (float)b;
-        return;
-    }
-    o0 = (float)v0;
-    o1 = (float)v1;
+    if (gauss_f32_exact_try(w0, w1, p, o0, o1)) exact_pair_f32(w0, w1, p.scale_d, p.off_d, p.exact, o0, o1);
 }
 
 // Lognormal (extension a18): x = exp(m + s*z) * scale + displ.

@@ -152,6 +152,86 @@ __device__ __forceinline__ void st_group_mis(T* p, const T o[4]) {
     }
 }
 
+
+// Odd-element pair outputs, warp-shifted (PhiloxBody::mis): a lane that holds
+// NE consecutive outputs v[0..NE) starting one element below a 32-byte
+// boundary writes v[1..NE) plus its right neighbour's v[0] (by shuffle) as
+// whole 32-byte sectors; only the first lane stores its v[0] on its own and a
+// lane without a right neighbour ends with 16/8/4-byte pieces.  Every element
+// is written once, with full-sector stores except at the two ends of a
+// warp's run.
+template <typename T>
+__device__ __forceinline__ void st_bytes32(T* p, const T* e) {
+    if constexpr (sizeof(T) == 4) {
+        uint32_t b[8];
+        memcpy(b, e, 32);
+        asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(b[0]), "r"(b[1]), "r"(b[2]),
+                     "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(b[6]), "r"(b[7]) : "memory");
+    } else {
+        unsigned long long b[4];
+        memcpy(b, e, 32);
+        asm volatile("st.global.cs.v4.b64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3])
+                     : "memory");
+    }
+}
+template <typename T, int BYTES>
+__device__ __forceinline__ void st_piece(T* p, const T* e) {
+    if constexpr (BYTES == 16 && sizeof(T) == 4) {
+        uint32_t b[4];
+        memcpy(b, e, 16);
+        asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3])
+                     : "memory");
+    } else if constexpr (BYTES == 16) {
+        unsigned long long b[2];
+        memcpy(b, e, 16);
+        asm volatile("st.global.cs.v2.b64 [%0], {%1,%2};" ::"l"(p), "l"(b[0]), "l"(b[1]) : "memory");
+    } else if constexpr (BYTES == 8 && sizeof(T) == 4) {
+        uint32_t b[2];
+        memcpy(b, e, 8);
+        asm volatile("st.global.cs.v2.b32 [%0], {%1,%2};" ::"l"(p), "r"(b[0]), "r"(b[1]) : "memory");
+    } else if constexpr (BYTES == 8) {
+        unsigned long long b;
+        memcpy(&b, e, 8);
+        asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(p), "l"(b) : "memory");
+    } else {
+        uint32_t b;
+        memcpy(&b, e, 4);
+        asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(b) : "memory");
+    }
+}
+
+template <typename T, int NG>
+__device__ __forceinline__ void st_run_shift1(T* dst, const T (&o)[NG][4], T nxt, bool has_next, bool first) {
+    constexpr int NE = 4 * NG;
+    constexpr int PER = 32 / (int)sizeof(T);
+    const T* v = &o[0][0];
+    if (first) st_piece<T, sizeof(T)>(dst, v);
+    T* a = dst + 1;  // 32-byte aligned
+    if (has_next) {
+#pragma unroll
+        for (int c = 0; c < NE / PER; ++c) {
+            T e[PER];
+#pragma unroll
+            for (int k = 0; k < PER; ++k) e[k] = (1 + c * PER + k < NE) ? v[1 + c * PER + k] : nxt;
+            st_bytes32(a + c * PER, e);
+        }
+    } else {
+        constexpr int M = NE - 1, FULL = M / PER;
+#pragma unroll
+        for (int c = 0; c < FULL; ++c) st_bytes32(a + c * PER, v + 1 + c * PER);
+        int off = FULL * PER;  // M - off < PER elements left: 16, 8, 4-byte pieces
+        if constexpr ((M - FULL * PER) * sizeof(T) >= 16) {
+            st_piece<T, 16>(a + off, v + 1 + off);
+            off += 16 / sizeof(T);
+        }
+        if constexpr (((M - FULL * PER) * sizeof(T)) % 16 >= 8) {
+            st_piece<T, 8>(a + off, v + 1 + off);
+            off += 8 / sizeof(T);
+        }
+        if constexpr (((M - FULL * PER) * sizeof(T)) % 8 >= 4) st_piece<T, 4>(a + off, v + 1 + off);
+    }
+}
+
 // Aligned path (SHIFT = 0) of one body launch; MIS: pair transforms whose
 // body starts one element below a 32-byte boundary (a separate instantiation
 // so the common loop keeps its register allocation).
@@ -167,11 +247,23 @@ __device__ __forceinline__ void philox_body_aligned(const PhiloxBody& a, uint32_
     const uint32_t gstep = gstride * BPT;
     const uint32_t gfull = a.ngroups - a.ngroups % BPT;
     T* dst = body + (size_t)4 * BPT * gtid;
-    auto store = [&](T* d, T (&o)[BPT][4]) {
-        if constexpr (MIS) {
+    if constexpr (MIS) {
+        // warp-uniform passes (the shuffle needs every lane); a lane's BPT
+        // groups follow its left neighbour's, lane 31's right neighbour is
+        // in the next warp
+        const uint32_t lane = threadIdx.x & 31;
+        for (uint32_t base = (gtid - lane) * BPT; base < gfull; base += gstep, dst += (size_t)4 * gstep) {
+            const uint32_t g0 = base + lane * BPT;
+            const bool valid = g0 < gfull;
+            T o[BPT][4];
 #pragma unroll
-            for (int j = 0; j < BPT; ++j) st_group_mis(d + 4 * j, o[j]);
-        } else if constexpr (sizeof(T) == 4) {
+            for (int j = 0; j < BPT; ++j) xform4<X>(philox_block_pre(a.k0, a.k1, a.c0 + g0 + j, a.pre), a.p, o[j]);
+            const T nxt = __shfl_down_sync(0xffffffffu, o[0][0], 1);
+            if (valid) st_run_shift1<T, BPT>(dst, o, nxt, lane != 31 && g0 + BPT < gfull, lane == 0);
+        }
+    } else {
+    auto store = [&](T* d, T (&o)[BPT][4]) {
+        if constexpr (sizeof(T) == 4) {
 #pragma unroll
             for (int j = 0; j < BPT; j += 2) st_group2(d + 4 * j, o[j], o[j + 1]);
         } else {
@@ -210,6 +302,7 @@ __device__ __forceinline__ void philox_body_aligned(const PhiloxBody& a, uint32_
             store(dst, o);
         }
     }
+    }
     if (gtid == gstride - 1) {
         for (uint32_t g = gfull; g < a.ngroups; ++g) {
             T o[4];
@@ -222,18 +315,14 @@ __device__ __forceinline__ void philox_body_aligned(const PhiloxBody& a, uint32_
     }
 }
 
-template <int X, int SHIFT>
+// MIS: the odd-element pair-output variant (PhiloxBody::mis), a separate
+// kernel instantiation so the common kernels keep their register counts.
+template <int X, int SHIFT, bool MIS = false>
 __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, uint32_t gstride) {
     using T = typename XformTraits<X>::T;
     T* __restrict__ body = static_cast<T*>(a.out);
     if constexpr (SHIFT == 0) {
-        if constexpr (XformTraits<X>::kPair) {
-            if (a.mis) {
-                philox_body_aligned<X, true>(a, gtid, gstride);
-                return;
-            }
-        }
-        philox_body_aligned<X, false>(a, gtid, gstride);
+        philox_body_aligned<X, MIS>(a, gtid, gstride);
     } else {
         // Warp-cooperative funnel.  Lane l of a warp pass computes blocks
         // 4l..4l+3 of the tile and takes block 4l+4 (the first block of lane
@@ -272,10 +361,23 @@ __device__ __forceinline__ void philox_body(const PhiloxBody& a, uint32_t gtid, 
             for (int j = 0; j < BPT; ++j) xform4<X>(funnel<SHIFT>(w[j], w[j + 1]), a.p, o[j]);
             T* dst = body + (size_t)4 * gb;
             const uint32_t nvalid = lane == 31 ? 2 : BPT;  // groups of this lane inside the pass
-            if (XformTraits<X>::kPair && a.mis != 0u) {
+            if constexpr (MIS) {
+                // odd-element pair output: whole lanes shift their run by one
+                // element (st_run_shift1); a lane cut by the end of the data
+                // stores group by group (its first element again: same value)
+                const T nxt = __shfl_down_sync(0xffffffffu, o[0][0], 1);
+                const bool full = gb + nvalid <= a.ngroups;
+                const bool has_next = lane < 31 && gb + BPT < a.ngroups;
+                if (full && lane < 31) {
+                    st_run_shift1<T, BPT>(dst, o, nxt, has_next, lane == 0);
+                } else if (full) {
+                    const T(&o2)[2][4] = *reinterpret_cast<const T(*)[2][4]>(&o[0][0]);
+                    st_run_shift1<T, 2>(dst, o2, nxt, false, false);
+                } else {
 #pragma unroll
-                for (int j = 0; j < BPT; ++j)
-                    if (j < (int)nvalid && gb + j < a.ngroups) st_group_mis(dst + 4 * j, o[j]);
+                    for (int j = 0; j < BPT; ++j)
+                        if (j < (int)nvalid && gb + j < a.ngroups) st_group_mis(dst + 4 * j, o[j]);
+                }
             } else if (nvalid == BPT && gb + BPT <= a.ngroups) {
                 if constexpr (sizeof(T) == 4) {
                     st_group2(dst, o[0], o[1]);
@@ -308,8 +410,9 @@ constexpr int philox_min_blocks() {
                                            : 0;
 }
 
-template <int X, int SHIFT>
-__global__ void __launch_bounds__(kPhiloxThreads, philox_min_blocks<X, SHIFT>()) philox_kernel(const PhiloxBody a) {
+template <int X, int SHIFT, bool MIS = false>
+__global__ void __launch_bounds__(kPhiloxThreads, MIS ? 0 : philox_min_blocks<X, SHIFT>())
+    philox_kernel(const PhiloxBody a) {
     xform_prologue<X>(a.p);
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gstride = gridDim.x * blockDim.x;
@@ -317,7 +420,7 @@ __global__ void __launch_bounds__(kPhiloxThreads, philox_min_blocks<X, SHIFT>())
         using T = typename XformTraits<X>::T;
         philox_scalar_range<X>(a.s, a.p, static_cast<T*>(a.out) - a.s.i0, gtid, gstride);
     }
-    if (a.ngroups) philox_body<X, SHIFT>(a, gtid, gstride);
+    if (a.ngroups) philox_body<X, SHIFT, MIS>(a, gtid, gstride);
 }
 
 // ------------------------------------------------------------- segments

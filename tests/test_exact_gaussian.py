@@ -87,7 +87,7 @@ def test_exact_route_rounding_test_bounds_and_cancellation_cases():
     """The fp32 exact route skips the correction tables unless the fp64
     value sits within its error bound of an fp32 rounding boundary.  The
     bounds it uses are the worst approximation errors measured over the
-    whole domains; they must be tiny (a few fp64 ulps).  Outputs stay
+    whole domains; they must be tiny (the short fp64 forms: ~2^-44).  Outputs stay
     bit-identical where the affine cancels (mean ~ -z * sd), the case the
     bound's |v| terms exist for."""
     import ctypes
@@ -97,7 +97,7 @@ def test_exact_route_rounding_test_bounds_and_cancellation_cases():
     esc = ctypes.c_uint64()
     P._lib.check(P._lib.lib.prng_exact_tables_bounds(b, ctypes.byref(esc)))
     print(json.dumps({"exact_bounds": {"rel_log": b[0], "abs_sincos": b[1], "escapes": esc.value}}))
-    assert 0 <= b[0] < 2.0 ** -48 and 0 <= b[1] < 2.0 ** -50
+    assert 0 <= b[0] < 2.0 ** -40 and 0 <= b[1] < 2.0 ** -40
     st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 2024)
     for mean, sd in ((-1.0, 1.0), (1.0, 1.0), (1e-3, 1e-3), (-3.0, 1.0), (0.0, 1e-30), (1e20, 1e20)):
         n = 1 << 20

@@ -16,6 +16,8 @@ W = {
     "gauss_f32": ("philox", lambda: P.Gaussian(0.0, 1.0), torch.float32),
     "gauss_f32_acc": ("philox", lambda: P.Gaussian(0.0, 1.0, method="accurate"), torch.float32),
     "gauss_f32_exact": ("philox", lambda: P.Gaussian(0.0, 1.0, method="exact"), torch.float32),
+    "gauss_f32_precise": ("philox", lambda: P.Gaussian(0.0, 1.0, method="precise"), torch.float32),
+    "logn_f32_precise": ("philox", lambda: P.Lognormal(method="precise"), torch.float32),
     "gauss_f64_exact": ("philox", lambda: P.Gaussian(0.0, 1.0, "fp64", "exact"), torch.float64),
     "gauss_f64": ("philox", lambda: P.Gaussian(0.0, 1.0, "fp64"), torch.float64),
     "logn_f32": ("philox", lambda: P.Lognormal(), torch.float32),
