@@ -10,13 +10,13 @@
 //     unrolled leaves), amounts = raw * (target / raw_sum) (or target / m),
 //     particle_sum = pairwise sum of amounts;
 //   * per event: deposits = np.unique + np.bincount over the particles' hits
-//     in order, i.e. cells sorted ascending and each cell's amounts summed
-//     sequentially in hit order: a stable segmented radix sort (CUB) by cell
-//     over the cell-id bits only, then one sequential run-sum per unique
-//     cell, compacted with a block scan into one packed array (a count pass,
-//     a device scan of the counts, a write pass) so the host copies back
-//     exactly the deposits.
-#include <cub/cub.cuh>
+//     in order, i.e. cells ascending and each cell's amounts summed
+//     sequentially in hit order: a shared-memory bitmap of the event's cells
+//     ranks them (no sort), one warp adds the amounts in hit order, and a
+//     decoupled look-back over the events' deposit counts packs the output
+//     in the same launch (calo_deposit_kernel) so the host copies back
+//     exactly the deposits.  No library kernels.
+#include <cuda/atomic>
 #include <cuda_runtime.h>
 
 #include <cstdarg>
@@ -216,41 +216,329 @@ __global__ void __launch_bounds__(32 * kNormWarps)
     if (lane == 0) particle_sums[p] = sum;
 }
 
-// One CTA per event over its cell-sorted hits.  COUNT pass: number of unique
-// cells per event.  WRITE pass: (cell, sequential run sum) compacted at the
-// event's packed offset dep_offsets[e] (exclusive scan of the counts).
-template <bool WRITE>
-__global__ void __launch_bounds__(kCaloThreads)
-    calo_reduce_kernel(const uint32_t* __restrict__ keys, const double* __restrict__ vals,
-                       const uint64_t* __restrict__ ev_off, uint64_t* __restrict__ counts,
-                       const uint64_t* __restrict__ dep_offsets, uint32_t* __restrict__ dep_cell,
-                       double* __restrict__ dep_energy) {
-    using Scan = cub::BlockScan<uint32_t, kCaloThreads>;
-    __shared__ typename Scan::TempStorage tmp;
-    __shared__ uint32_t carry;
-    const uint64_t beg = ev_off[blockIdx.x], end = ev_off[blockIdx.x + 1];
-    const uint64_t out0 = WRITE ? dep_offsets[blockIdx.x] : 0;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (uint64_t base = beg; base < end; base += kCaloThreads) {
-        const uint64_t i = base + threadIdx.x;
-        const uint32_t flag = (i < end && (i == beg || keys[i] != keys[i - 1])) ? 1u : 0u;
-        uint32_t idx, total;
-        Scan(tmp).ExclusiveSum(flag, idx, total);
-        if (WRITE && flag) {
-            const uint32_t key = keys[i];
-            double s = 0.0;  // np.bincount: 0.0, then += weights in input order
-            for (uint64_t k = i; k < end && keys[k] == key; ++k) s = __dadd_rn(s, vals[k]);
-            dep_cell[out0 + carry + idx] = key;
-            dep_energy[out0 + carry + idx] = s;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) carry += total;
-        __syncthreads();
+// ------------------------------------------------------------- deposits
+// Per event e (hits [ev_off[e], ev_off[e+1]) in hit order) the deposits are
+// np.unique(cells) ascending with np.bincount(inverse, weights=amounts)
+// (calosim.py:340-347): each unique cell's amounts summed sequentially in hit
+// order, starting from 0.0.  One CTA per event (events taken by ticket, in
+// order), and no sort:
+//  1. the event's cells are marked in a shared-memory bitmap over the window
+//     [lo, lo + 2^wbits) (atomicOr); a block scan of the 64-bit words'
+//     popcounts gives every marked cell its rank among the event's unique
+//     cells, i.e. its deposit slot in np.unique's ascending order;
+//  2. the event publishes its deposit count and finds its packed output
+//     offset by a decoupled look-back over the earlier events' counts (one
+//     pass: no separate count, scan and write launches);
+//  3. the hits, in stages of 1024, are split stably by slot & 7 into shared
+//     memory, and warp b adds bucket b's amounts to their slots' fp64 sums in
+//     hit order (eight walkers on disjoint slots); lanes of a step that hit
+//     the same cell (__match_any_sync) are added by the group's first lane
+//     in lane order, so every sum is the sequential one, bit for bit;
+//  4. the sums and the cells (decoded from the bitmap) are written packed.
+// A cell range wider than the window is covered by successive windows, each
+// starting at the smallest cell not yet covered; more unique cells than the
+// sums buffer holds take one walk per slot chunk.
+constexpr int kDepThreads = 256;
+constexpr int kDepWarps = kDepThreads / 32;
+constexpr uint32_t kDepMaxWinLog2 = 18;  // 2^18 cells: 32 KB bitmap + 16 KB ranks
+constexpr uint32_t kDepSlots = 4096;     // fp64 sums per walk (32 KB)
+constexpr uint32_t kDepStage = 1024;     // hits per split stage (12 KB)
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+struct DepSmem {
+    uint32_t red[2 * kDepWarps];
+    uint32_t scan[kDepWarps];
+    uint32_t event, total;
+    unsigned long long off;
+};
+
+// Block-wide min of the event's cells >= floor (0xFFFFFFFF: none) and max of all.
+__device__ void dep_minmax(DepSmem& s, const uint32_t* __restrict__ cells, uint64_t beg, uint64_t end,
+                           uint64_t floor, uint32_t& mn, uint32_t& mx) {
+    uint32_t a = 0xFFFFFFFFu, b = 0;
+    for (uint64_t i = beg + threadIdx.x; i < end; i += kDepThreads) {
+        const uint32_t c = cells[i];
+        if ((uint64_t)c >= floor && c < a) a = c;
+        b = c > b ? c : b;
     }
-    if (!WRITE && threadIdx.x == 0) counts[blockIdx.x] = carry;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+        b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    const uint32_t w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s.red[w] = a;
+        s.red[kDepWarps + w] = b;
+    }
+    __syncthreads();
+    a = s.red[0];
+    b = s.red[kDepWarps];
+#pragma unroll
+    for (int k = 1; k < kDepWarps; ++k) {
+        a = min(a, s.red[k]);
+        b = max(b, s.red[kDepWarps + k]);
+    }
+    __syncthreads();
+    mn = a;
+    mx = b;
 }
 
+// Marks the cells in [lo, lo + 64 nw) and ranks the words: pref[q] = set bits
+// in words < q.  Returns the window's unique-cell count (every thread).
+__device__ uint32_t dep_build_window(DepSmem& s, unsigned long long* bm, uint32_t* pref,
+                                     const uint32_t* __restrict__ cells, uint64_t beg, uint64_t end, uint32_t lo,
+                                     uint32_t nw) {
+    for (uint32_t q = threadIdx.x; q < nw; q += kDepThreads) bm[q] = 0ull;
+    __syncthreads();
+    const uint64_t span = 64ull * nw;
+    for (uint64_t i = beg + threadIdx.x; i < end; i += kDepThreads) {
+        const uint32_t c = cells[i];
+        if (c >= lo && (uint64_t)(c - lo) < span)  // 32-bit halves of the 64-bit words (little-endian)
+            atomicOr(reinterpret_cast<unsigned int*>(bm) + ((c - lo) >> 5), 1u << ((c - lo) & 31u));
+    }
+    __syncthreads();
+    // each thread owns a contiguous run of words; block exclusive scan of the runs' popcounts
+    const uint32_t per = (nw + kDepThreads - 1) / kDepThreads;
+    const uint32_t q0 = threadIdx.x * per, q1 = min(q0 + per, nw);
+    uint32_t mine = 0;
+    for (uint32_t q = q0; q < q1; ++q) mine += __popcll(bm[q]);
+    uint32_t inc = mine;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((int)lane >= o) inc += v;
+    }
+    if (lane == 31) s.scan[w] = inc;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kDepWarps; ++k) {
+        base += k < (int)w ? s.scan[k] : 0u;
+        total += s.scan[k];
+    }
+    uint32_t r = base + inc - mine;
+    for (uint32_t q = q0; q < q1; ++q) {
+        pref[q] = r;
+        r += __popcll(bm[q]);
+    }
+    __syncthreads();
+    return total;
+}
+
+__device__ __forceinline__ uint32_t dep_rank(const unsigned long long* bm, const uint32_t* pref, uint32_t rel) {
+    const uint32_t q = rel >> 6;
+    return pref[q] + __popcll(bm[q] & ((1ull << (rel & 63u)) - 1ull));
+}
+
+// Warp w walks its bucket's entries of a stage in order: sums[rs] += amount.
+// Lanes of a step that hit the same slot (__match_any_sync) are added by the
+// group's first lane in lane order, so every sum is the sequential one.
+__device__ __forceinline__ void dep_walk(double* sums, const uint32_t* st_slot, const double* st_amt, uint32_t cnt) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t t = 0; t < cnt; t += 32) {
+        const bool ok = t + lane < cnt;
+        const uint32_t rs = ok ? st_slot[t + lane] : 0u;
+        const double a = ok ? st_amt[t + lane] : 0.0;
+        const uint32_t m = __match_any_sync(0xffffffffu, ok ? rs : (0x80000000u | lane));
+        const bool grp = ok && (m & (m - 1u)) != 0u;
+        uint32_t dup = __ballot_sync(0xffffffffu, grp);
+        if (ok && !grp) sums[rs] = __dadd_rn(sums[rs], a);
+        if (dup) {
+            const bool lead = grp && (m & ((1u << lane) - 1u)) == 0u;
+            double acc = lead ? sums[rs] : 0.0;
+            while (dup) {
+                const int k = __ffs(dup) - 1;
+                dup &= dup - 1u;
+                const double ak = __shfl_sync(0xffffffffu, a, k);
+                if (lead && ((m >> k) & 1u)) acc = __dadd_rn(acc, ak);
+            }
+            if (lead) sums[rs] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+// sums[slot - s0] += amount over the event's hits in order, for the slots in
+// [s0, s0 + nslots) of the window at lo.  The hits go in stages of
+// kDepStage (warp w loads tiles 8w..8w+7 of the stage); each stage is split
+// stably by bucket = slot & 7 (ballots, per-tile counts, a scan per bucket)
+// into shared memory, and warp b walks bucket b: eight walkers on disjoint
+// slots, each seeing its hits in hit order.
+constexpr uint32_t kDepTilesPerWarp = kDepStage / 32 / kDepWarps;
+static_assert(kDepStage == 32 * 32 && kDepWarps == 8 && kDepTilesPerWarp * 8 == 32,
+              "the split scans 8 buckets x 32 tiles with 256 threads");
+
+__device__ void dep_sum_slots(double* sums, uint32_t* st_slot, double* st_amt, uint32_t* tcnt,
+                              const unsigned long long* bm, const uint32_t* pref, const uint32_t* __restrict__ cells,
+                              const double* __restrict__ amts, uint64_t beg, uint64_t end, uint32_t lo,
+                              uint64_t span, uint32_t s0, uint32_t nslots) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t j = threadIdx.x; j < nslots; j += kDepThreads) sums[j] = 0.0;
+    // tcnt: [bucket][tile] counts (8 x 32), then the per-bucket totals
+    uint32_t* wsum = tcnt + kDepWarps * (kDepStage / 32);
+    for (uint64_t h0 = beg; h0 < end; h0 += kDepStage) {
+        uint32_t rs[kDepTilesPerWarp], rk[kDepTilesPerWarp];
+        double av[kDepTilesPerWarp];
+#pragma unroll
+        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
+            const uint64_t i = h0 + (uint64_t)(w * kDepTilesPerWarp + k) * 32 + lane;
+            uint32_t r = 0xFFFFFFFFu;
+            av[k] = 0.0;
+            if (i < end) {
+                const uint32_t c = cells[i];
+                av[k] = amts[i];
+                if (c >= lo && (uint64_t)(c - lo) < span) {
+                    const uint32_t q = dep_rank(bm, pref, c - lo) - s0;
+                    if (q < nslots) r = q;
+                }
+            }
+            rs[k] = r;
+        }
+#pragma unroll
+        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
+            const uint32_t bk = rs[k] == 0xFFFFFFFFu ? 8u : (rs[k] & 7u);
+            uint32_t mine = 0;
+#pragma unroll
+            for (uint32_t b = 0; b < 8; ++b) {
+                const uint32_t m = __ballot_sync(0xffffffffu, bk == b);
+                if (bk == b) mine = __popc(m & lt);
+                if (lane == b) tcnt[b * 32 + w * kDepTilesPerWarp + k] = __popc(m);
+            }
+            rk[k] = mine;
+        }
+        __syncthreads();
+        // exclusive scan of the counts in [bucket][tile] order (thread t: bucket
+        // t / 32 = its warp, tile t % 32): every (bucket, tile) gets its first
+        // position, bucket w's run starts where warp w's entries start
+        const uint32_t v = tcnt[threadIdx.x];
+        uint32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+            if ((int)lane >= o) inc += x;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        uint32_t wstart = 0;
+#pragma unroll
+        for (uint32_t b = 0; b < kDepWarps; ++b) wstart += b < w ? wsum[b] : 0u;
+        const uint32_t wcount = wsum[w];
+        tcnt[threadIdx.x] = wstart + inc - v;
+        __syncthreads();
+#pragma unroll
+        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
+            if (rs[k] != 0xFFFFFFFFu) {
+                const uint32_t pos = tcnt[(rs[k] & 7u) * 32 + w * kDepTilesPerWarp + k] + rk[k];
+                st_slot[pos] = rs[k];
+                st_amt[pos] = av[k];
+            }
+        }
+        __syncthreads();
+        dep_walk(sums, st_slot + wstart, st_amt + wstart, wcount);
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kDepThreads, 1)
+    calo_deposit_kernel(const uint32_t* __restrict__ cells, const double* __restrict__ amts,
+                        const uint64_t* __restrict__ ev_off, uint32_t nevents, uint32_t cell_bits,
+                        uint32_t wbits, unsigned long long* status, unsigned int* ticket, uint32_t* __restrict__ dep_cell,
+                        double* __restrict__ dep_energy, uint64_t* __restrict__ dep_offsets) {
+    extern __shared__ __align__(16) unsigned char dep_dyn[];
+    __shared__ DepSmem s;
+    const uint32_t nwords = 1u << (wbits - 6);
+    double* sums = reinterpret_cast<double*>(dep_dyn);
+    unsigned long long* bm = reinterpret_cast<unsigned long long*>(dep_dyn + kDepSlots * sizeof(double));
+    uint32_t* pref = reinterpret_cast<uint32_t*>(bm + nwords);
+    double* st_amt = reinterpret_cast<double*>(dep_dyn + kDepSlots * sizeof(double) +
+                                               (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint32_t)));
+    uint32_t* st_slot = reinterpret_cast<uint32_t*>(st_amt + kDepStage);
+    uint32_t* tcnt = st_slot + kDepStage;
+    const uint64_t win = 64ull * nwords;
+    const bool wide = cell_bits == 0 || cell_bits > wbits;  // ids may lie beyond the first window
+    for (;;) {
+        if (threadIdx.x == 0) s.event = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t e = s.event;
+        if (e >= nevents) return;
+        const uint64_t beg = ev_off[e], end = ev_off[e + 1];
+        uint32_t lo = 0, cmax = (uint32_t)(win - 1);  // ids < 2^wbits: one window from 0, no min/max pass
+        if (end > beg && wide) dep_minmax(s, cells, beg, end, 0, lo, cmax);
+        auto words_of = [&](uint32_t wlo) {  // words covering [wlo, min(cmax, wlo + win - 1)]
+            const uint64_t top = (uint64_t)cmax - wlo;
+            return top >= win ? nwords : (uint32_t)(top >> 6) + 1u;
+        };
+        const bool single = end == beg || (uint64_t)cmax - lo < win;
+        // 1. count (a single window stays built for the walk)
+        uint64_t total = 0;
+        uint32_t first_u = 0;
+        if (end > beg) {
+            uint32_t wlo = lo;
+            for (;;) {
+                const uint32_t u = dep_build_window(s, bm, pref, cells, beg, end, wlo, words_of(wlo));
+                if (wlo == lo) first_u = u;
+                total += u;
+                if (single || (uint64_t)wlo + win > cmax) break;
+                uint32_t unused;
+                dep_minmax(s, cells, beg, end, (uint64_t)wlo + win, wlo, unused);  // exists: cmax qualifies
+            }
+        }
+        // 2. packed offset: decoupled look-back over the earlier events
+        if (threadIdx.x == 0) {
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(status[e]);
+            unsigned long long prefix = 0;
+            if (e > 0) {
+                me.store(kLbAgg | total, cuda::memory_order_relaxed);
+                for (uint32_t j = e - 1;; --j) {
+                    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> st(status[j]);
+                    unsigned long long v;
+                    while (((v = st.load(cuda::memory_order_relaxed)) >> 62) == 0ull) __nanosleep(64);
+                    prefix += v & kLbVal;
+                    if ((v & kLbInc) || j == 0) break;
+                }
+            }
+            me.store(kLbInc | (prefix + total), cuda::memory_order_relaxed);
+            dep_offsets[e] = prefix;
+            if (e == nevents - 1) dep_offsets[nevents] = prefix + total;
+            s.off = prefix;
+        }
+        __syncthreads();
+        const uint64_t off = s.off;
+        // 3-4. walks and packed writes, window by window
+        if (end > beg) {
+            uint64_t base = off;
+            uint32_t wlo = lo;
+            for (;;) {
+                const uint32_t nw = words_of(wlo);
+                const uint32_t u = wlo == lo && single ? first_u : dep_build_window(s, bm, pref, cells, beg, end, wlo, nw);
+                for (uint32_t s0 = 0; s0 < u; s0 += kDepSlots) {
+                    const uint32_t ns = min(kDepSlots, u - s0);
+                    dep_sum_slots(sums, st_slot, st_amt, tcnt, bm, pref, cells, amts, beg, end, wlo, 64ull * nw, s0, ns);
+                    for (uint32_t j = threadIdx.x; j < ns; j += kDepThreads) dep_energy[base + s0 + j] = sums[j];
+                    __syncthreads();
+                }
+                for (uint32_t q = threadIdx.x; q < nw; q += kDepThreads) {
+                    unsigned long long bits = bm[q];
+                    uint64_t r = base + pref[q];
+                    while (bits) {
+                        const int b = __ffsll((long long)bits) - 1;
+                        bits &= bits - 1ull;
+                        dep_cell[r++] = wlo + 64u * q + (uint32_t)b;
+                    }
+                }
+                base += u;
+                __syncthreads();
+                if (single || (uint64_t)wlo + win > cmax) break;
+                uint32_t unused;
+                dep_minmax(s, cells, beg, end, (uint64_t)wlo + win, wlo, unused);  // exists: cmax qualifies
+            }
+        }
+        __syncthreads();  // s.event / s.off are rewritten by the next ticket
+    }
+}
 }  // namespace
 
 int prng_detail_fail(int code, const char* msg);  // api.cu: the prng_last_error() slot
@@ -285,31 +573,13 @@ int prng_calo_hits(const float* batch, const prng_calo_particle_t* particles, ui
 }
 
 namespace {
-struct DepositScratch {
-    size_t keys, vals, counts, sort_temp, scan_temp, total;
-};
-
-DepositScratch deposit_layout(uint64_t total_hits, uint32_t nevents) {
-    size_t sort_temp = 0, scan_temp = 0;
-    cub::DeviceSegmentedRadixSort::SortPairs(nullptr, sort_temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                             (const double*)nullptr, (double*)nullptr, (int64_t)total_hits,
-                                             (int64_t)nevents, (const uint64_t*)nullptr, (const uint64_t*)nullptr);
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                  (int64_t)nevents + 1);
-    auto up = [](size_t b) { return (b + 255) / 256 * 256; };
-    DepositScratch d;
-    d.keys = up(total_hits * sizeof(uint32_t));
-    d.vals = up(total_hits * sizeof(double));
-    d.counts = up(((size_t)nevents + 1) * sizeof(uint64_t));
-    d.sort_temp = up(sort_temp);
-    d.scan_temp = up(scan_temp);
-    d.total = d.keys + d.vals + d.counts + d.sort_temp + d.scan_temp;
-    return d;
-}
+// Scratch: one look-back status word per event and the ticket counter.
+size_t deposit_scratch(uint32_t nevents) { return ((size_t)nevents + 1) * sizeof(unsigned long long); }
 }  // namespace
 
 size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents) {
-    return deposit_layout(total_hits, nevents).total;
+    (void)total_hits;
+    return deposit_scratch(nevents);
 }
 
 int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64_t total_hits,
@@ -317,39 +587,37 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
                       size_t scratch_bytes, uint32_t* dep_cell, double* dep_energy, uint64_t* dep_offsets,
                       void* stream) {
     if (nevents == 0) return PRNG_OK;
-    if (!hit_cell || !hit_amount || !event_hit_offsets || !dep_cell || !dep_energy || !dep_offsets)
+    if ((total_hits && (!hit_cell || !hit_amount)) || !event_hit_offsets || !dep_cell || !dep_energy || !dep_offsets)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
     if (cell_bits > 32) return calo_fail(PRNG_ERR_INVALID_PARAMETER, "cell_bits must be <= 32");
-    const DepositScratch L = deposit_layout(total_hits, nevents);
-    if (!scratch || scratch_bytes < L.total)
-        return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", L.total);
+    const size_t need = deposit_scratch(nevents);
+    if (!scratch || scratch_bytes < need)
+        return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", need);
     cudaStream_t s = (cudaStream_t)stream;
-    char* p = static_cast<char*>(scratch);
-    uint32_t* keys_out = reinterpret_cast<uint32_t*>(p);
-    p += L.keys;
-    double* vals_out = reinterpret_cast<double*>(p);
-    p += L.vals;
-    uint64_t* counts = reinterpret_cast<uint64_t*>(p);
-    p += L.counts;
-    void* sort_temp = p;
-    p += L.sort_temp;
-    void* scan_temp = p;
-    size_t sort_bytes = L.sort_temp, scan_bytes = L.scan_temp;
-    const int end_bit = cell_bits == 0 ? 32 : (int)cell_bits;  // keys < 2^cell_bits: fewer radix passes
-    if (total_hits) {
-        cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairs(sort_temp, sort_bytes, hit_cell, keys_out,
-                                                                 hit_amount, vals_out, (int64_t)total_hits,
-                                                                 (int64_t)nevents, event_hit_offsets,
-                                                                 event_hit_offsets + 1, 0, end_bit, s);
-        if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "segmented sort: %s", cudaGetErrorString(e));
-    }
-    cudaMemsetAsync(counts + nevents, 0, sizeof(uint64_t), s);
-    calo_reduce_kernel<false><<<nevents, kCaloThreads, 0, s>>>(keys_out, vals_out, event_hit_offsets, counts,
-                                                               nullptr, nullptr, nullptr);
-    cudaError_t e = cub::DeviceScan::ExclusiveSum(scan_temp, scan_bytes, counts, dep_offsets, (int64_t)nevents + 1, s);
-    if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "offset scan: %s", cudaGetErrorString(e));
-    calo_reduce_kernel<true><<<nevents, kCaloThreads, 0, s>>>(keys_out, vals_out, event_hit_offsets, nullptr,
-                                                              dep_offsets, dep_cell, dep_energy);
+    // bitmap window: the whole cell-id range when it has <= 2^18 ids
+    const uint32_t b = cell_bits == 0 ? 32u : cell_bits;
+    const uint32_t wbits = b < 6u ? 6u : (b > kDepMaxWinLog2 ? kDepMaxWinLog2 : b);
+    const uint32_t nwords = 1u << (wbits - 6);
+    const size_t smem = kDepSlots * sizeof(double) + (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint32_t)) +
+                        kDepStage * (sizeof(double) + sizeof(uint32_t)) +
+                        (kDepWarps * (kDepStage / 32) + kDepWarps) * sizeof(uint32_t);
+    int dev = 0, nsm = 0, per_sm = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(calo_deposit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, calo_deposit_kernel, kDepThreads, smem);
+    if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "calo deposit setup: %s", cudaGetErrorString(e));
+    const uint64_t slots = (uint64_t)(per_sm > 0 ? per_sm : 1) * (uint64_t)nsm;
+    const uint32_t grid = (uint32_t)(slots < nevents ? slots : nevents);
+    unsigned long long* status = static_cast<unsigned long long*>(scratch);
+    e = cudaMemsetAsync(status, 0, need, s);
+    if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(e));
+    calo_deposit_kernel<<<grid, kDepThreads, smem, s>>>(hit_cell, hit_amount, event_hit_offsets, nevents, cell_bits,
+                                                        wbits, status,
+                                                        reinterpret_cast<unsigned int*>(status + nevents), dep_cell,
+                                                        dep_energy, dep_offsets);
     e = cudaGetLastError();
     return e == cudaSuccess ? PRNG_OK : calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(e));
 }
