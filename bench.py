@@ -22,9 +22,12 @@ torchrun WORLD_SIZE must equal --gpus.  Before timing, every rank checks
 its first and last 4096 samples against the CPU oracle at its global
 offset r*n (the single-stream slice rule, rngburn.py:70-73).
 
-`--impl reference`: the reference's own CPU path (oracle/cpu_baseline.py:
-the compiled portarng kernel core from oracle/_ref driven the way
-burn_once(..., Parallel(ncpu)) drives it) on this host's cores, rank 0 only.
+`--impl reference`: the reference's own CPU path, unmodified: stock
+portarng rngburn.burn_once(PHILOX4X32X10, Uniform(0,1,fp32), "buffer",
+Parallel(ncpu)) from the staged reference (baseline/_ref/pkg, its compiled
+Cython core selected) on this host's cores, rank 0 only; plus the
+"hostdirect"/Serial cycle and single-thread kernel_bench rates as secondary
+numbers.
 """
 
 from __future__ import annotations

@@ -33,6 +33,21 @@ det = C.Detector(geom, {"electron": C.Parameterization("electron", 40, 90, np.li
                                                        np.full(8, 0.125))})
 ev = C.synth_single_electron_events(20, 777)
 C.simulate_events(ev, det, P.seed_engine(P.EngineKind.PHILOX4X32X10, 777), min_batch=500)
+# deposit kernel on its own: two windows (ids up to 2^20), > 4096 unique cells, one hot cell
+from paper_2109_01329_b200 import _lib
+rng = np.random.default_rng(3)
+cells = np.concatenate([rng.integers(0, 1 << 20, 6000), np.full(300, 77), rng.integers(0, 64, 50)]).astype(np.int32)
+offs = torch.tensor([0, 6000, 6000, 6300, 6350], dtype=torch.int64, device="cuda")
+d_c = torch.from_numpy(cells).cuda()
+d_a = torch.rand(len(cells), dtype=torch.float64, device="cuda")
+nb = _lib.lib.prng_calo_deposit_scratch_bytes(len(cells), 4)
+scr = torch.empty(nb, dtype=torch.uint8, device="cuda")
+oc = torch.empty(len(cells), dtype=torch.int32, device="cuda")
+oe = torch.empty(len(cells), dtype=torch.float64, device="cuda")
+oo = torch.empty(5, dtype=torch.int64, device="cuda")
+_lib.check(_lib.lib.prng_calo_deposit(d_c.data_ptr(), d_a.data_ptr(), len(cells), offs.data_ptr(), 4, 0, scr.data_ptr(),
+                                      nb, oc.data_ptr(), oe.data_ptr(), oo.data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream))
 g = X.TaskGraph()
 b = g.create_buffer(10007)
 g.submit_with_accessors(X.uniform_generate_kernel(ph, b.id, "fp32"), [(b, X.AccessMode.READ_WRITE)])
