@@ -12,10 +12,11 @@
 //   * per event: deposits = np.unique + np.bincount over the particles' hits
 //     in order, i.e. cells ascending and each cell's amounts summed
 //     sequentially in hit order: a shared-memory bitmap of the event's cells
-//     ranks them (no sort), one warp adds the amounts in hit order, and a
-//     decoupled look-back over the events' deposit counts packs the output
-//     in the same launch (calo_deposit_kernel) so the host copies back
-//     exactly the deposits.  No library kernels.
+//     ranks them, a counting sort by rank buckets the hits, each bucket is
+//     put back in hit order and summed by one thread, and a decoupled
+//     look-back over the events' deposit counts packs the output in the same
+//     launch (calo_deposit_kernel) so the host copies back exactly the
+//     deposits.  No library kernels.
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
@@ -221,36 +222,64 @@ __global__ void __launch_bounds__(32 * kNormWarps)
 // np.unique(cells) ascending with np.bincount(inverse, weights=amounts)
 // (calosim.py:340-347): each unique cell's amounts summed sequentially in hit
 // order, starting from 0.0.  One CTA per event (events taken by ticket, in
-// order), and no sort:
+// order), no sort of the hits and no serial walk:
 //  1. the event's cells are marked in a shared-memory bitmap over the window
 //     [lo, lo + 2^wbits) (atomicOr); a block scan of the 64-bit words'
-//     popcounts gives every marked cell its rank among the event's unique
-//     cells, i.e. its deposit slot in np.unique's ascending order;
+//     popcounts ranks every marked cell among the event's unique cells: its
+//     deposit slot, in np.unique's ascending order;
 //  2. the event publishes its deposit count and finds its packed output
 //     offset by a decoupled look-back over the earlier events' counts (one
 //     pass: no separate count, scan and write launches);
-//  3. the hits, in stages of 1024, are split stably by slot & 7 into shared
-//     memory, and warp b adds bucket b's amounts to their slots' fp64 sums in
-//     hit order (eight walkers on disjoint slots); lanes of a step that hit
-//     the same cell (__match_any_sync) are added by the group's first lane
-//     in lane order, so every sum is the sequential one, bit for bit;
-//  4. the sums and the cells (decoded from the bitmap) are written packed.
-// A cell range wider than the window is covered by successive windows, each
-// starting at the smallest cell not yet covered; more unique cells than the
-// sums buffer holds take one walk per slot chunk.
+//  3. a counting sort of the hits by slot (count, block scan, fill) leaves
+//     each slot's hit indices in one bucket; the fill's atomics order a
+//     bucket arbitrarily, so the slot's thread puts it back in hit order
+//     (insertion sort: buckets hold ~1.4 hits here) and adds the amounts
+//     sequentially; buckets of more than 32 hits are ordered by the whole
+//     CTA (bitonic network) and summed by one thread.  Every sum is the
+//     sequential one, bit for bit;
+//  4. the sums and the cells are written packed at the event's offset.
+// Events of up to 8192 hits keep their counters and indices in shared
+// memory (16-bit), larger ones in the caller's scratch (32-bit).  A cell
+// range wider than the window is covered by successive windows, each
+// starting at the smallest cell not yet covered.
 constexpr int kDepThreads = 256;
 constexpr int kDepWarps = kDepThreads / 32;
-constexpr uint32_t kDepMaxWinLog2 = 18;  // 2^18 cells: 32 KB bitmap + 16 KB ranks
-constexpr uint32_t kDepSlots = 4096;     // fp64 sums per walk (32 KB)
-constexpr uint32_t kDepStage = 1024;     // hits per split stage (12 KB)
+constexpr uint32_t kDepMaxWinLog2 = 18;  // 2^18 cells: 32 KB bitmap + 8 KB of 16-bit ranks
+constexpr uint32_t kDepRankBlock = 256;  // words per 32-bit rank base
+constexpr uint32_t kDepCap = 8192;       // hits per event indexed in shared memory
+constexpr uint32_t kDepSmall = 32;       // larger buckets are ordered by the whole CTA
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
 
 struct DepSmem {
     uint32_t red[2 * kDepWarps];
     uint32_t scan[kDepWarps];
-    uint32_t event, total;
+    uint32_t event, nbig;
     unsigned long long off;
+    uint32_t rbase[(1u << kDepMaxWinLog2) / 64 / kDepRankBlock];
+    uint32_t big[kDepCap / (kDepSmall + 1) + 1];  // slots with large buckets (shared-memory path)
 };
+
+// Block-wide exclusive scan of one value per thread; *total = the sum.
+__device__ uint32_t dep_block_scan(DepSmem& s, uint32_t v, uint32_t* total) {
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
+        if ((int)lane >= o) inc += x;
+    }
+    if (lane == 31) s.scan[w] = inc;
+    __syncthreads();
+    uint32_t base = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kDepWarps; ++k) {
+        base += k < (int)w ? s.scan[k] : 0u;
+        tot += s.scan[k];
+    }
+    __syncthreads();
+    *total = tot;
+    return base + inc - v;
+}
 
 // Block-wide min of the event's cells >= floor (0xFFFFFFFF: none) and max of all.
 __device__ void dep_minmax(DepSmem& s, const uint32_t* __restrict__ cells, uint64_t beg, uint64_t end,
@@ -284,9 +313,11 @@ __device__ void dep_minmax(DepSmem& s, const uint32_t* __restrict__ cells, uint6
     mx = b;
 }
 
-// Marks the cells in [lo, lo + 64 nw) and ranks the words: pref[q] = set bits
-// in words < q.  Returns the window's unique-cell count (every thread).
-__device__ uint32_t dep_build_window(DepSmem& s, unsigned long long* bm, uint32_t* pref,
+// Marks the cells in [lo, lo + 64 nw) and ranks the words: the rank of word
+// q (set bits in words < q) is rbase[q / 256] plus the 16-bit offset
+// (pref[q] - rbase) mod 2^16 (a block of 256 words holds <= 16384 bits).
+// Returns the window's unique-cell count.
+__device__ uint32_t dep_build_window(DepSmem& s, unsigned long long* bm, uint16_t* pref,
                                      const uint32_t* __restrict__ cells, uint64_t beg, uint64_t end, uint32_t lo,
                                      uint32_t nw) {
     for (uint32_t q = threadIdx.x; q < nw; q += kDepThreads) bm[q] = 0ull;
@@ -298,165 +329,193 @@ __device__ uint32_t dep_build_window(DepSmem& s, unsigned long long* bm, uint32_
             atomicOr(reinterpret_cast<unsigned int*>(bm) + ((c - lo) >> 5), 1u << ((c - lo) & 31u));
     }
     __syncthreads();
-    // each thread owns a contiguous run of words; block exclusive scan of the runs' popcounts
     const uint32_t per = (nw + kDepThreads - 1) / kDepThreads;
-    const uint32_t q0 = threadIdx.x * per, q1 = min(q0 + per, nw);
+    const uint32_t q0 = min(threadIdx.x * per, nw), q1 = min(q0 + per, nw);
     uint32_t mine = 0;
     for (uint32_t q = q0; q < q1; ++q) mine += __popcll(bm[q]);
-    uint32_t inc = mine;
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
-        if ((int)lane >= o) inc += v;
-    }
-    if (lane == 31) s.scan[w] = inc;
-    __syncthreads();
-    uint32_t base = 0, total = 0;
-#pragma unroll
-    for (int k = 0; k < kDepWarps; ++k) {
-        base += k < (int)w ? s.scan[k] : 0u;
-        total += s.scan[k];
-    }
-    uint32_t r = base + inc - mine;
+    uint32_t total;
+    uint32_t r = dep_block_scan(s, mine, &total);
     for (uint32_t q = q0; q < q1; ++q) {
-        pref[q] = r;
+        if ((q & (kDepRankBlock - 1)) == 0) s.rbase[q / kDepRankBlock] = r;
+        pref[q] = (uint16_t)r;
         r += __popcll(bm[q]);
     }
     __syncthreads();
     return total;
 }
 
-__device__ __forceinline__ uint32_t dep_rank(const unsigned long long* bm, const uint32_t* pref, uint32_t rel) {
+__device__ __forceinline__ uint32_t dep_rank(const DepSmem& s, const unsigned long long* bm, const uint16_t* pref,
+                                             uint32_t rel) {
     const uint32_t q = rel >> 6;
-    return pref[q] + __popcll(bm[q] & ((1ull << (rel & 63u)) - 1ull));
+    const uint32_t b = s.rbase[q / kDepRankBlock];
+    return b + (((uint32_t)pref[q] - b) & 0xFFFFu) + __popcll(bm[q] & ((1ull << (rel & 63u)) - 1ull));
 }
 
-// Warp w walks its bucket's entries of a stage in order: sums[rs] += amount.
-// Lanes of a step that hit the same slot (__match_any_sync) are added by the
-// group's first lane in lane order, so every sum is the sequential one.
-__device__ __forceinline__ void dep_walk(double* sums, const uint32_t* st_slot, const double* st_amt, uint32_t cnt) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t t = 0; t < cnt; t += 32) {
-        const bool ok = t + lane < cnt;
-        const uint32_t rs = ok ? st_slot[t + lane] : 0u;
-        const double a = ok ? st_amt[t + lane] : 0.0;
-        const uint32_t m = __match_any_sync(0xffffffffu, ok ? rs : (0x80000000u | lane));
-        const bool grp = ok && (m & (m - 1u)) != 0u;
-        uint32_t dup = __ballot_sync(0xffffffffu, grp);
-        if (ok && !grp) sums[rs] = __dadd_rn(sums[rs], a);
-        if (dup) {
-            const bool lead = grp && (m & ((1u << lane) - 1u)) == 0u;
-            double acc = lead ? sums[rs] : 0.0;
-            while (dup) {
-                const int k = __ffs(dup) - 1;
-                dup &= dup - 1u;
-                const double ak = __shfl_sync(0xffffffffu, a, k);
-                if (lead && ((m >> k) & 1u)) acc = __dadd_rn(acc, ak);
-            }
-            if (lead) sums[rs] = acc;
-        }
-        __syncwarp();
+// Bucket storage.  Shared memory: 16-bit counters packed in pairs and 16-bit
+// hit indices; global (events of more than kDepCap hits): 32-bit, in scratch.
+struct DepIdxShared {
+    uint32_t* cnt2;
+    uint16_t* lst;
+    uint32_t* big;
+    __device__ uint32_t add(uint32_t sl) const {
+        const uint32_t sh = (sl & 1u) << 4;
+        return (atomicAdd(&cnt2[sl >> 1], 1u << sh) >> sh) & 0xFFFFu;
     }
+    __device__ uint32_t get(uint32_t sl) const { return (cnt2[sl >> 1] >> ((sl & 1u) << 4)) & 0xFFFFu; }
+    __device__ uint32_t idx(uint32_t p) const { return lst[p]; }
+    __device__ void put(uint32_t p, uint32_t h) const { lst[p] = (uint16_t)h; }
+    // zero / exclusive-scan the first u counters (whole 32-bit words per thread)
+    __device__ void zero(uint32_t u) const {
+        for (uint32_t w = threadIdx.x; w < (u + 1) / 2; w += kDepThreads) cnt2[w] = 0u;
+    }
+    __device__ void scan(DepSmem& s, uint32_t u) const {
+        const uint32_t nw = (u + 1) / 2, per = (nw + kDepThreads - 1) / kDepThreads;
+        const uint32_t w0 = min(threadIdx.x * per, nw), w1 = min(w0 + per, nw);
+        uint32_t mine = 0;
+        for (uint32_t w = w0; w < w1; ++w) mine += (cnt2[w] & 0xFFFFu) + (cnt2[w] >> 16);
+        uint32_t total;
+        uint32_t r = dep_block_scan(s, mine, &total);
+        for (uint32_t w = w0; w < w1; ++w) {
+            const uint32_t v = cnt2[w];
+            const uint32_t a = r, b = r + (v & 0xFFFFu);
+            cnt2[w] = a | (b << 16);
+            r = b + (v >> 16);
+        }
+    }
+};
+
+struct DepIdxGlobal {
+    uint32_t* cnt;
+    uint32_t* lst;
+    uint32_t* big;
+    __device__ uint32_t add(uint32_t sl) const { return atomicAdd(&cnt[sl], 1u); }
+    __device__ uint32_t get(uint32_t sl) const { return cnt[sl]; }
+    __device__ uint32_t idx(uint32_t p) const { return lst[p]; }
+    __device__ void put(uint32_t p, uint32_t h) const { lst[p] = h; }
+    __device__ void zero(uint32_t u) const {
+        for (uint32_t w = threadIdx.x; w < u; w += kDepThreads) cnt[w] = 0u;
+    }
+    __device__ void scan(DepSmem& s, uint32_t u) const {
+        const uint32_t per = (u + kDepThreads - 1) / kDepThreads;
+        const uint32_t w0 = min(threadIdx.x * per, u), w1 = min(w0 + per, u);
+        uint32_t mine = 0;
+        for (uint32_t w = w0; w < w1; ++w) mine += cnt[w];
+        uint32_t total;
+        uint32_t r = dep_block_scan(s, mine, &total);
+        for (uint32_t w = w0; w < w1; ++w) {
+            const uint32_t v = cnt[w];
+            cnt[w] = r;
+            r += v;
+        }
+    }
+};
+
+// Sequential fp64 sum of the amounts of bucket [st, en) (hit order), with
+// the loads issued eight at a time.
+template <class IX>
+__device__ double dep_bucket_sum(const IX& ix, const double* __restrict__ amts, uint64_t beg, uint32_t st,
+                                 uint32_t en) {
+    double acc = 0.0;  // np.bincount: 0.0, then += weights in input order
+    uint32_t p = st;
+    for (; p + 8 <= en; p += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = amts[beg + ix.idx(p + j)];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc = __dadd_rn(acc, v[j]);
+    }
+    for (; p < en; ++p) acc = __dadd_rn(acc, amts[beg + ix.idx(p)]);
+    return acc;
 }
 
-// sums[slot - s0] += amount over the event's hits in order, for the slots in
-// [s0, s0 + nslots) of the window at lo.  The hits go in stages of
-// kDepStage (warp w loads tiles 8w..8w+7 of the stage); each stage is split
-// stably by bucket = slot & 7 (ballots, per-tile counts, a scan per bucket)
-// into shared memory, and warp b walks bucket b: eight walkers on disjoint
-// slots, each seeing its hits in hit order.
-constexpr uint32_t kDepTilesPerWarp = kDepStage / 32 / kDepWarps;
-static_assert(kDepStage == 32 * 32 && kDepWarps == 8 && kDepTilesPerWarp * 8 == 32,
-              "the split scans 8 buckets x 32 tiles with 256 threads");
-
-__device__ void dep_sum_slots(double* sums, uint32_t* st_slot, double* st_amt, uint32_t* tcnt,
-                              const unsigned long long* bm, const uint32_t* pref, const uint32_t* __restrict__ cells,
-                              const double* __restrict__ amts, uint64_t beg, uint64_t end, uint32_t lo,
-                              uint64_t span, uint32_t s0, uint32_t nslots) {
-    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    for (uint32_t j = threadIdx.x; j < nslots; j += kDepThreads) sums[j] = 0.0;
-    // tcnt: [bucket][tile] counts (8 x 32), then the per-bucket totals
-    uint32_t* wsum = tcnt + kDepWarps * (kDepStage / 32);
-    for (uint64_t h0 = beg; h0 < end; h0 += kDepStage) {
-        uint32_t rs[kDepTilesPerWarp], rk[kDepTilesPerWarp];
-        double av[kDepTilesPerWarp];
-#pragma unroll
-        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
-            const uint64_t i = h0 + (uint64_t)(w * kDepTilesPerWarp + k) * 32 + lane;
-            uint32_t r = 0xFFFFFFFFu;
-            av[k] = 0.0;
-            if (i < end) {
-                const uint32_t c = cells[i];
-                av[k] = amts[i];
-                if (c >= lo && (uint64_t)(c - lo) < span) {
-                    const uint32_t q = dep_rank(bm, pref, c - lo) - s0;
-                    if (q < nslots) r = q;
-                }
-            }
-            rs[k] = r;
-        }
-#pragma unroll
-        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
-            const uint32_t bk = rs[k] == 0xFFFFFFFFu ? 8u : (rs[k] & 7u);
-            uint32_t mine = 0;
-#pragma unroll
-            for (uint32_t b = 0; b < 8; ++b) {
-                const uint32_t m = __ballot_sync(0xffffffffu, bk == b);
-                if (bk == b) mine = __popc(m & lt);
-                if (lane == b) tcnt[b * 32 + w * kDepTilesPerWarp + k] = __popc(m);
-            }
-            rk[k] = mine;
-        }
-        __syncthreads();
-        // exclusive scan of the counts in [bucket][tile] order (thread t: bucket
-        // t / 32 = its warp, tile t % 32): every (bucket, tile) gets its first
-        // position, bucket w's run starts where warp w's entries start
-        const uint32_t v = tcnt[threadIdx.x];
-        uint32_t inc = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, inc, o);
-            if ((int)lane >= o) inc += x;
-        }
-        if (lane == 31) wsum[w] = inc;
-        __syncthreads();
-        uint32_t wstart = 0;
-#pragma unroll
-        for (uint32_t b = 0; b < kDepWarps; ++b) wstart += b < w ? wsum[b] : 0u;
-        const uint32_t wcount = wsum[w];
-        tcnt[threadIdx.x] = wstart + inc - v;
-        __syncthreads();
-#pragma unroll
-        for (uint32_t k = 0; k < kDepTilesPerWarp; ++k) {
-            if (rs[k] != 0xFFFFFFFFu) {
-                const uint32_t pos = tcnt[(rs[k] & 7u) * 32 + w * kDepTilesPerWarp + k] + rk[k];
-                st_slot[pos] = rs[k];
-                st_amt[pos] = av[k];
-            }
-        }
-        __syncthreads();
-        dep_walk(sums, st_slot + wstart, st_amt + wstart, wcount);
+// Deposits of the window at lo (u unique cells, ranked in bm/pref) written
+// at out + [0, u): counting sort of the hits by slot, then per-slot
+// sequential sums in hit order.
+template <class IX>
+__device__ void dep_window(DepSmem& s, const IX& ix, const unsigned long long* bm, const uint16_t* pref,
+                           const uint32_t* __restrict__ cells, const double* __restrict__ amts, uint64_t beg,
+                           uint64_t end, uint32_t lo, uint64_t span, uint32_t u, uint32_t* __restrict__ out_cell,
+                           double* __restrict__ out_energy) {
+    const uint32_t nh = (uint32_t)(end - beg);
+    ix.zero(u);
+    if (threadIdx.x == 0) s.nbig = 0;
+    __syncthreads();
+    for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
+        const uint32_t c = cells[beg + h];
+        if (c >= lo && (uint64_t)(c - lo) < span) ix.add(dep_rank(s, bm, pref, c - lo));
     }
     __syncthreads();
+    ix.scan(s, u);
+    __syncthreads();
+    for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
+        const uint32_t c = cells[beg + h];
+        if (c >= lo && (uint64_t)(c - lo) < span) ix.put(ix.add(dep_rank(s, bm, pref, c - lo)), h);
+    }
+    __syncthreads();
+    // counters now hold each bucket's end; bucket sl = [end(sl - 1), end(sl))
+    for (uint32_t sl = threadIdx.x; sl < u; sl += kDepThreads) {
+        const uint32_t st = sl ? ix.get(sl - 1) : 0u, en = ix.get(sl);
+        if (en - st > kDepSmall) {
+            ix.big[atomicAdd(&s.nbig, 1u)] = sl;
+            continue;
+        }
+        for (uint32_t i = st + 1; i < en; ++i) {  // insertion sort back into hit order
+            const uint32_t v = ix.idx(i);
+            uint32_t j = i;
+            for (; j > st && ix.idx(j - 1) > v; --j) ix.put(j, ix.idx(j - 1));
+            ix.put(j, v);
+        }
+        out_energy[sl] = dep_bucket_sum(ix, amts, beg, st, en);
+        out_cell[sl] = cells[beg + ix.idx(st)];
+    }
+    __syncthreads();
+    const uint32_t nbig = s.nbig;
+    for (uint32_t b = 0; b < nbig; ++b) {
+        const uint32_t sl = ix.big[b];
+        const uint32_t st = sl ? ix.get(sl - 1) : 0u, en = ix.get(sl), k = en - st;
+        uint32_t P = 2;
+        while (P < k) P <<= 1;
+        // bitonic network with every comparator ascending (the first stage of
+        // each merge compares mirrored pairs); positions >= k act as +inf
+        for (uint32_t size = 2; size <= P; size <<= 1) {
+            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+                const uint32_t lg = __ffs(stride) - 1;
+                for (uint32_t t = threadIdx.x; t < P / 2; t += kDepThreads) {
+                    const uint32_t blk = t >> lg, o = t & (stride - 1);
+                    const uint32_t i = stride == size >> 1 ? blk * size + o : blk * 2 * stride + o;
+                    const uint32_t j = stride == size >> 1 ? blk * size + size - 1 - o : i + stride;
+                    if (j < k) {
+                        const uint32_t a = ix.idx(st + i), c = ix.idx(st + j);
+                        if (a > c) {
+                            ix.put(st + i, c);
+                            ix.put(st + j, a);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        if (threadIdx.x == 0) {
+            out_energy[sl] = dep_bucket_sum(ix, amts, beg, st, en);
+            out_cell[sl] = cells[beg + ix.idx(st)];
+        }
+        __syncthreads();
+    }
 }
 
-__global__ void __launch_bounds__(kDepThreads, 1)
+__global__ void __launch_bounds__(kDepThreads, 3)
     calo_deposit_kernel(const uint32_t* __restrict__ cells, const double* __restrict__ amts,
-                        const uint64_t* __restrict__ ev_off, uint32_t nevents, uint32_t cell_bits,
-                        uint32_t wbits, unsigned long long* status, unsigned int* ticket, uint32_t* __restrict__ dep_cell,
-                        double* __restrict__ dep_energy, uint64_t* __restrict__ dep_offsets) {
+                        const uint64_t* __restrict__ ev_off, uint32_t nevents, uint32_t cell_bits, uint32_t wbits,
+                        unsigned long long* status, unsigned int* ticket, uint32_t* gidx, uint64_t total_hits,
+                        uint32_t* __restrict__ dep_cell, double* __restrict__ dep_energy,
+                        uint64_t* __restrict__ dep_offsets) {
     extern __shared__ __align__(16) unsigned char dep_dyn[];
     __shared__ DepSmem s;
     const uint32_t nwords = 1u << (wbits - 6);
-    double* sums = reinterpret_cast<double*>(dep_dyn);
-    unsigned long long* bm = reinterpret_cast<unsigned long long*>(dep_dyn + kDepSlots * sizeof(double));
-    uint32_t* pref = reinterpret_cast<uint32_t*>(bm + nwords);
-    double* st_amt = reinterpret_cast<double*>(dep_dyn + kDepSlots * sizeof(double) +
-                                               (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint32_t)));
-    uint32_t* st_slot = reinterpret_cast<uint32_t*>(st_amt + kDepStage);
-    uint32_t* tcnt = st_slot + kDepStage;
+    unsigned long long* bm = reinterpret_cast<unsigned long long*>(dep_dyn);
+    uint32_t* cnt2 = reinterpret_cast<uint32_t*>(bm + nwords);
+    uint16_t* lst = reinterpret_cast<uint16_t*>(cnt2 + kDepCap / 2);
+    uint16_t* pref = lst + kDepCap;
     const uint64_t win = 64ull * nwords;
     const bool wide = cell_bits == 0 || cell_bits > wbits;  // ids may lie beyond the first window
     for (;;) {
@@ -472,7 +531,7 @@ __global__ void __launch_bounds__(kDepThreads, 1)
             return top >= win ? nwords : (uint32_t)(top >> 6) + 1u;
         };
         const bool single = end == beg || (uint64_t)cmax - lo < win;
-        // 1. count (a single window stays built for the walk)
+        // 1. count (a single window stays built for step 3)
         uint64_t total = 0;
         uint32_t first_u = 0;
         if (end > beg) {
@@ -507,30 +566,24 @@ __global__ void __launch_bounds__(kDepThreads, 1)
         }
         __syncthreads();
         const uint64_t off = s.off;
-        // 3-4. walks and packed writes, window by window
+        // 3-4. per-window counting sort, per-slot sums, packed writes
         if (end > beg) {
+            const bool small = end - beg <= kDepCap;
+            const DepIdxShared ixs{cnt2, lst, s.big};
+            const DepIdxGlobal ixg{gidx + beg, gidx + total_hits + beg, gidx + 2 * total_hits + beg};
             uint64_t base = off;
             uint32_t wlo = lo;
             for (;;) {
                 const uint32_t nw = words_of(wlo);
-                const uint32_t u = wlo == lo && single ? first_u : dep_build_window(s, bm, pref, cells, beg, end, wlo, nw);
-                for (uint32_t s0 = 0; s0 < u; s0 += kDepSlots) {
-                    const uint32_t ns = min(kDepSlots, u - s0);
-                    dep_sum_slots(sums, st_slot, st_amt, tcnt, bm, pref, cells, amts, beg, end, wlo, 64ull * nw, s0, ns);
-                    for (uint32_t j = threadIdx.x; j < ns; j += kDepThreads) dep_energy[base + s0 + j] = sums[j];
-                    __syncthreads();
-                }
-                for (uint32_t q = threadIdx.x; q < nw; q += kDepThreads) {
-                    unsigned long long bits = bm[q];
-                    uint64_t r = base + pref[q];
-                    while (bits) {
-                        const int b = __ffsll((long long)bits) - 1;
-                        bits &= bits - 1ull;
-                        dep_cell[r++] = wlo + 64u * q + (uint32_t)b;
-                    }
-                }
+                const uint32_t u =
+                    wlo == lo && single ? first_u : dep_build_window(s, bm, pref, cells, beg, end, wlo, nw);
+                if (small)
+                    dep_window(s, ixs, bm, pref, cells, amts, beg, end, wlo, 64ull * nw, u, dep_cell + base,
+                               dep_energy + base);
+                else
+                    dep_window(s, ixg, bm, pref, cells, amts, beg, end, wlo, 64ull * nw, u, dep_cell + base,
+                               dep_energy + base);
                 base += u;
-                __syncthreads();
                 if (single || (uint64_t)wlo + win > cmax) break;
                 uint32_t unused;
                 dep_minmax(s, cells, beg, end, (uint64_t)wlo + win, wlo, unused);  // exists: cmax qualifies
@@ -573,13 +626,17 @@ int prng_calo_hits(const float* batch, const prng_calo_particle_t* particles, ui
 }
 
 namespace {
-// Scratch: one look-back status word per event and the ticket counter.
-size_t deposit_scratch(uint32_t nevents) { return ((size_t)nevents + 1) * sizeof(unsigned long long); }
+// Scratch: one look-back status word per event, the ticket counter, and the
+// 32-bit bucket arrays of events with more than kDepCap hits (counters,
+// hit indices, large-bucket list: total_hits entries each).
+size_t deposit_status_bytes(uint32_t nevents) { return ((size_t)nevents + 1) * sizeof(unsigned long long); }
+size_t deposit_scratch(uint64_t total_hits, uint32_t nevents) {
+    return deposit_status_bytes(nevents) + 3 * (size_t)total_hits * sizeof(uint32_t);
+}
 }  // namespace
 
 size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents) {
-    (void)total_hits;
-    return deposit_scratch(nevents);
+    return deposit_scratch(total_hits, nevents);
 }
 
 int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64_t total_hits,
@@ -590,7 +647,7 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     if ((total_hits && (!hit_cell || !hit_amount)) || !event_hit_offsets || !dep_cell || !dep_energy || !dep_offsets)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
     if (cell_bits > 32) return calo_fail(PRNG_ERR_INVALID_PARAMETER, "cell_bits must be <= 32");
-    const size_t need = deposit_scratch(nevents);
+    const size_t need = deposit_scratch(total_hits, nevents);
     if (!scratch || scratch_bytes < need)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", need);
     cudaStream_t s = (cudaStream_t)stream;
@@ -598,9 +655,8 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     const uint32_t b = cell_bits == 0 ? 32u : cell_bits;
     const uint32_t wbits = b < 6u ? 6u : (b > kDepMaxWinLog2 ? kDepMaxWinLog2 : b);
     const uint32_t nwords = 1u << (wbits - 6);
-    const size_t smem = kDepSlots * sizeof(double) + (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint32_t)) +
-                        kDepStage * (sizeof(double) + sizeof(uint32_t)) +
-                        (kDepWarps * (kDepStage / 32) + kDepWarps) * sizeof(uint32_t);
+    const size_t smem = (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint16_t)) +
+                        kDepCap / 2 * sizeof(uint32_t) + kDepCap * sizeof(uint16_t);
     int dev = 0, nsm = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -612,12 +668,13 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     const uint64_t slots = (uint64_t)(per_sm > 0 ? per_sm : 1) * (uint64_t)nsm;
     const uint32_t grid = (uint32_t)(slots < nevents ? slots : nevents);
     unsigned long long* status = static_cast<unsigned long long*>(scratch);
-    e = cudaMemsetAsync(status, 0, need, s);
+    e = cudaMemsetAsync(status, 0, deposit_status_bytes(nevents), s);
     if (e != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(e));
     calo_deposit_kernel<<<grid, kDepThreads, smem, s>>>(hit_cell, hit_amount, event_hit_offsets, nevents, cell_bits,
                                                         wbits, status,
-                                                        reinterpret_cast<unsigned int*>(status + nevents), dep_cell,
-                                                        dep_energy, dep_offsets);
+                                                        reinterpret_cast<unsigned int*>(status + nevents),
+                                                        reinterpret_cast<uint32_t*>(status + nevents + 1), total_hits,
+                                                        dep_cell, dep_energy, dep_offsets);
     e = cudaGetLastError();
     return e == cudaSuccess ? PRNG_OK : calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(e));
 }
