@@ -622,9 +622,9 @@ def run_c5_full(args):
                                                        "segment launch, deposition kernels and D2H of results"},
         "e2e": {"value": nev / sec, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(res["cells"].nbytes + res["energy"].nbytes)},
-        # per step: control-word segments, batch segments, hits, normalise, 3 radix
-        # passes (cell_bits = 18), count, 2 scan kernels, write (profiles/r1_launches_bench_c5_full.csv)
-        "cpu_baseline": cpu, "gpu_launches": 11,
+        # per step: one control-word segment launch, then per 2048-event chunk: batch segments,
+        # hits, normalise, deposit (profiles/r2_launches_c5_full.csv)
+        "cpu_baseline": cpu, "gpu_launches": 1 + 4 * ((nev + 2047) // 2048),
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -201,7 +201,8 @@ int prng_calo_hits(const float *batch, const prng_calo_particle_t *particles, ui
  * cell_bits: every cell id is < 2^cell_bits (0 = 32); ids < 2^18 are ranked
  * in one shared-memory bitmap window per event, wider ranges in several.
  * scratch: prng_calo_deposit_scratch_bytes(total_hits, nevents) bytes of
- * device memory (look-back state; zeroed by the call on `stream`). */
+ * device memory (look-back state, zeroed by the call on `stream`, and the
+ * bucket arrays of events with more than 8192 hits).  One kernel launch. */
 size_t prng_calo_deposit_scratch_bytes(uint64_t total_hits, uint32_t nevents);
 int prng_calo_deposit(const uint32_t *hit_cell, const double *hit_amount, uint64_t total_hits,
                       const uint64_t *event_hit_offsets, uint32_t nevents, uint32_t cell_bits, void *scratch,
