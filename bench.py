@@ -577,12 +577,12 @@ def run_c5_full(args):
     # the next allocates, so the pinned-host caching allocator needs two
     # sets of result buffers before it stops calling cudaHostAlloc.
     for _ in range(max(2, args.warmup)):
-        final, res = C.simulate_events(events, det, st, dicts=False)
+        final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=args.c5_chunk)
     torch.cuda.synchronize()
     ts = []
     for _ in range(max(1, args.steps)):
         t0 = time.perf_counter()
-        final, res = C.simulate_events(events, det, st, dicts=False)
+        final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=args.c5_chunk)
         torch.cuda.synchronize()
         ts.append(time.perf_counter() - t0)
     log("c5_full step ms: " + " ".join(f"{t * 1e3:.2f}" for t in ts))
@@ -618,13 +618,14 @@ def run_c5_full(args):
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32->fp32 (fp64 deposition)", "data": "synthetic single-electron events (seed 777)",
         "config": {"workload": f"{nev} events, 190000 cells / 24 regions, min_batch 200000",
+                   "chunk_events": args.c5_chunk,
                    "total_hits": total_hits, "timing": "wall clock of simulate_events incl. planning, "
                                                        "segment launch, deposition kernels and D2H of results"},
         "e2e": {"value": nev / sec, "unit": "events/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(res["cells"].nbytes + res["energy"].nbytes)},
         # per step: one control-word segment launch, then per 2048-event chunk: batch segments,
         # hits, normalise, deposit (profiles/r2_launches_c5_full.csv)
-        "cpu_baseline": cpu, "gpu_launches": 1 + 4 * ((nev + 2047) // 2048),
+        "cpu_baseline": cpu, "gpu_launches": 1 + 4 * ((nev + args.c5_chunk - 1) // args.c5_chunk),
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -1014,6 +1015,7 @@ def main():
     ap.add_argument("--sweep", action="store_true", help="also run the C4 batch-size sweep (CUDA-graph timed)")
     ap.add_argument("--sweep-max", type=int, default=32)
     ap.add_argument("--events", type=int, default=10000, help="C5 event count")
+    ap.add_argument("--c5-chunk", type=int, default=2048, help="C5 events per pipelined chunk")
     args = ap.parse_args()
     if args.gpus is not None and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args.gpus)

@@ -1250,6 +1250,14 @@ int prng_philox4x32x10_uniform_f32_segments(uint32_t k0, uint32_t k1, const prng
     return PRNG_OK;
 }
 
+#ifdef PRNG_TRACE_CTA
+int prng_diag_cta_trace(unsigned long long* host, int n) {  // diagnostics build only
+    return cudaMemcpyFromSymbol(host, prng::g_cta_trace, sizeof(unsigned long long) * 3 * (size_t)n) == cudaSuccess
+               ? PRNG_OK
+               : PRNG_ERR_CUDA;
+}
+#endif
+
 int prng_diag_write_probe(void* out, uint64_t bytes, void* stream) {
     DeviceGuard guard_;
     if (!out || ((uintptr_t)out & 31u) || (bytes & 63u))

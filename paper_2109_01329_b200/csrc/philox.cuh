@@ -410,9 +410,26 @@ constexpr int philox_min_blocks() {
                                            : 0;
 }
 
+#ifdef PRNG_TRACE_CTA  // diagnostics build only (tools/cta_residency.py): per-CTA SM id, start, end (ns)
+__device__ unsigned long long g_cta_trace[8192][3];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
 template <int X, int SHIFT, bool MIS = false>
 __global__ void __launch_bounds__(kPhiloxThreads, MIS ? 0 : philox_min_blocks<X, SHIFT>())
     philox_kernel(const PhiloxBody a) {
+#ifdef PRNG_TRACE_CTA
+    if (threadIdx.x == 0 && blockIdx.x < 8192) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta_trace[blockIdx.x][0] = smid;
+        g_cta_trace[blockIdx.x][1] = gtimer();
+    }
+#endif
     xform_prologue<X>(a.p);
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t gstride = gridDim.x * blockDim.x;
@@ -421,6 +438,10 @@ __global__ void __launch_bounds__(kPhiloxThreads, MIS ? 0 : philox_min_blocks<X,
         philox_scalar_range<X>(a.s, a.p, static_cast<T*>(a.out) - a.s.i0, gtid, gstride);
     }
     if (a.ngroups) philox_body<X, SHIFT, MIS>(a, gtid, gstride);
+#ifdef PRNG_TRACE_CTA
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < 8192) g_cta_trace[blockIdx.x][2] = gtimer();
+#endif
 }
 
 // ------------------------------------------------------------- segments
