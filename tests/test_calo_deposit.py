@@ -113,3 +113,36 @@ def test_deposit_small_cell_bits_and_many_events():
     assert np.array_equal(np.diff(got_o), counts)
     assert np.array_equal(got_c, want_c)
     assert np.array_equal(got_e.view(np.uint64), want_e.view(np.uint64))
+
+
+def test_deposit_narrow_ids_and_bucket_storage():
+    """Ids below 2^cell_bits with cell_bits <= 18 (one window from 0, no
+    min/max pass): empty, single-hit, exactly-8192-hit (the largest event
+    with shared-memory buckets) next to 8193-hit (32-bit buckets in scratch),
+    hot-cell (> 32 hits per bucket: the CTA-wide bitonic order) and
+    all-unique events; the same events again with cell_bits = 0."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2109_01329_b200 import _lib
+    rng = np.random.default_rng(11)
+    mag = lambda n: rng.choice([1.0, 1e-3, 1e8, 3e15], size=n) * rng.random(n)  # noqa: E731
+    ev = [(np.zeros(0, np.uint32), np.zeros(0)), (np.array([5], np.uint32), np.array([2.5]))]
+    ev.append((rng.integers(0, 1 << 18, 8192).astype(np.uint32), mag(8192)))
+    ev.append((rng.integers(0, 1 << 18, 8193).astype(np.uint32), mag(8193)))
+    ev.append((rng.choice(np.array([7, 70000, (1 << 18) - 1], np.uint32), 4000), mag(4000)))
+    ev.append((np.full(3000, 12345, np.uint32), mag(3000)))
+    ev.append((rng.permutation(6000).astype(np.uint32) * 41, mag(6000)))
+    for _ in range(300):
+        n = int(rng.integers(0, 300))
+        ev.append((rng.integers(0, 1 << 18, n).astype(np.uint32), mag(n)))
+    cells = np.concatenate([c for c, _ in ev]).astype(np.uint32)
+    amts = np.concatenate([a for _, a in ev]).astype(np.float64)
+    offs = np.zeros(len(ev) + 1, dtype=np.int64)
+    np.cumsum([len(c) for c, _ in ev], out=offs[1:])
+    want_c, want_e, counts = _numpy_deposits(cells, amts, offs)
+    for cell_bits in (18, 0):
+        got_c, got_e, got_o = _run(_lib.lib, torch, cells, amts, offs, cell_bits)
+        assert np.array_equal(np.diff(got_o), counts)
+        assert np.array_equal(got_c, want_c)
+        assert np.array_equal(got_e.view(np.uint64), want_e.view(np.uint64))
