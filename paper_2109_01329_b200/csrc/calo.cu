@@ -78,16 +78,20 @@ __global__ void __launch_bounds__(kCaloThreads)
     }
 }
 
-// numpy's pairwise sum evaluated by a warp: the recursion's leaves (runs of
-// <= 128 elements, each summed exactly as np_pairwise_sum's leaf branch) are
-// independent, so lane 0 lists them once per particle (iterative DFS),
-// lane l sums leaves l, l + 32, ..., and lane 0 adds the leaf sums back up the
-// same binary tree (iterative post-order walk).  Bit-identical to
-// np_pairwise_sum.  All stacks live in shared memory: no local memory, so
-// the kernel carries no per-thread stack reservation.
+// numpy's pairwise sum evaluated by a warp.  The recursion tree of
+// np_pairwise_sum(., n) depends only on n: lane 0 walks it once per particle
+// (iterative DFS, leaves in order) and records its leaves (runs of <= 128
+// elements) and its internal nodes with their children and depth; the leaves
+// are summed four at a time, eight lanes per leaf (numpy's eight accumulator
+// chains), and the internal nodes are added level by level from the deepest
+// (every node is left + right of values already computed, so the order
+// across independent nodes changes nothing).  Bit-identical to
+// np_pairwise_sum; both sums of a particle reuse the tree.  Trees of more
+// than kNormMaxLeaves leaves (particles of > ~16k hits) are summed by lane 0
+// on the fly (np_leaf_sum / combine_serial).
 constexpr int kNormWarps = 4;
-constexpr int kNormMaxLeaves = 512;  // n <= ~28k per particle in the list; larger: leaves summed by lane 0
-constexpr int kNormStack = 48;      // tree depth <= log2(n / 64) + 1 < 48 for any 64-bit n
+constexpr int kNormMaxLeaves = 256;
+constexpr int kNormStack = 48;  // tree depth <= log2(n / 64) + 1 < 48 for any 64-bit n
 
 __device__ __forceinline__ uint64_t pw_split(uint64_t n) {  // numpy: n2 = n / 2; n2 -= n2 % 8
     const uint64_t n2 = n / 2;
@@ -95,54 +99,73 @@ __device__ __forceinline__ uint64_t pw_split(uint64_t n) {  // numpy: n2 = n / 2
 }
 
 struct NormWarpSmem {
-    uint64_t leaf_off[kNormMaxLeaves];
-    uint32_t leaf_len[kNormMaxLeaves];
-    double leaf_val[kNormMaxLeaves];
+    double val[2 * kNormMaxLeaves];  // leaf k at [k], internal node i at [kNormMaxLeaves + i]
+    uint32_t leaf_off[kNormMaxLeaves];
+    uint16_t child[kNormMaxLeaves][2];  // ids into val
+    uint8_t leaf_len[kNormMaxLeaves];
+    uint8_t depth[kNormMaxLeaves];
     uint64_t st_off[kNormStack], st_n[kNormStack];
-    double st_left[kNormStack];
+    uint32_t st_slot[kNormStack];  // DFS: child slot to fill (node * 2 + side, or ~0 for the root)
+    uint8_t st_depth[kNormStack];
+    double st_left[kNormStack];    // combine_serial
     uint32_t st_stage[kNormStack];
 };
 
-// Lane 0: the leaves of np_pairwise_sum(., n) in order; returns their count
-// (entries past kNormMaxLeaves are counted, not stored).
-__device__ uint32_t list_leaves(NormWarpSmem& m, uint64_t n) {
-    int sp = 0;
-    uint32_t k = 0;
+struct NormTree {
+    uint32_t nleaves, nnodes, maxdepth;
+    bool listed;
+};
+
+// Lane 0: np_pairwise_sum's tree over n elements.
+__device__ NormTree build_tree(NormWarpSmem& m, uint64_t n) {
+    NormTree t{0, 0, 0, true};
+    int sp = 1;
     m.st_off[0] = 0;
     m.st_n[0] = n;
-    sp = 1;
+    m.st_slot[0] = ~0u;
+    m.st_depth[0] = 0;
     while (sp) {
         --sp;
         const uint64_t off = m.st_off[sp], len = m.st_n[sp];
+        const uint32_t slot = m.st_slot[sp];
+        const uint32_t d = m.st_depth[sp];
+        uint32_t id;
         if (len <= 128) {
-            if (k < (uint32_t)kNormMaxLeaves) {
-                m.leaf_off[k] = off;
-                m.leaf_len[k] = (uint32_t)len;
+            id = t.nleaves++;
+            if (id < (uint32_t)kNormMaxLeaves) {
+                m.leaf_off[id] = (uint32_t)off;
+                m.leaf_len[id] = (uint8_t)len;
             }
-            ++k;
-            continue;
+        } else {
+            const uint32_t i = t.nnodes++;
+            id = kNormMaxLeaves + i;
+            const uint64_t n2 = pw_split(len);
+            if (i < (uint32_t)kNormMaxLeaves) m.depth[i] = (uint8_t)d;
+            t.maxdepth = d > t.maxdepth ? d : t.maxdepth;
+            m.st_off[sp] = off + n2;  // right, popped second
+            m.st_n[sp] = len - n2;
+            m.st_slot[sp] = 2 * i + 1;
+            m.st_depth[sp] = (uint8_t)(d + 1);
+            ++sp;
+            m.st_off[sp] = off;  // left, popped first: leaves come out in order
+            m.st_n[sp] = n2;
+            m.st_slot[sp] = 2 * i;
+            m.st_depth[sp] = (uint8_t)(d + 1);
+            ++sp;
         }
-        const uint64_t n2 = pw_split(len);
-        m.st_off[sp] = off + n2;
-        m.st_n[sp] = len - n2;
-        ++sp;
-        m.st_off[sp] = off;
-        m.st_n[sp] = n2;
-        ++sp;
+        if (slot != ~0u && (slot >> 1) < (uint32_t)kNormMaxLeaves) m.child[slot >> 1][slot & 1u] = (uint16_t)id;
     }
-    return k;
+    t.listed = t.nleaves <= (uint32_t)kNormMaxLeaves;
+    return t;
 }
 
-// Lane 0: res = left + right at every internal node of np_pairwise_sum's
-// tree over n elements; leaves take leaf_val[] in order (listed) or are
-// summed on the fly from a (too many leaves for the list).
-__device__ double combine_leaves(NormWarpSmem& m, uint64_t n, const double* a, bool listed) {
-    int sp = 0;
-    uint32_t kk = 0;
+// Lane 0, trees too large for the lists: res = left + right at every
+// internal node, leaves summed on the fly (iterative post-order walk).
+__device__ double combine_serial(NormWarpSmem& m, uint64_t n, const double* a) {
+    int sp = 1;
     m.st_off[0] = 0;
     m.st_n[0] = n;
     m.st_stage[0] = 0;
-    sp = 1;
     for (;;) {
         const int t = sp - 1;
         if (m.st_n[t] > 128) {
@@ -153,7 +176,7 @@ __device__ double combine_leaves(NormWarpSmem& m, uint64_t n, const double* a, b
             ++sp;
             continue;
         }
-        double val = listed ? m.leaf_val[kk++] : np_leaf_sum(a + m.st_off[t], m.st_n[t]);
+        double val = np_leaf_sum(a + m.st_off[t], m.st_n[t]);
         --sp;
         for (;;) {  // deliver val to the parents
             if (sp == 0) return val;
@@ -174,14 +197,58 @@ __device__ double combine_leaves(NormWarpSmem& m, uint64_t n, const double* a, b
     }
 }
 
-__device__ double warp_pairwise_sum(NormWarpSmem& m, const double* a, uint64_t n, uint32_t nleaves, uint32_t lane) {
-    const bool listed = nleaves <= (uint32_t)kNormMaxLeaves;
-    if (listed) {
-        for (uint32_t i = lane; i < nleaves; i += 32) m.leaf_val[i] = np_leaf_sum(a + m.leaf_off[i], m.leaf_len[i]);
-        __syncwarp();
+// Four leaves per warp step, eight lanes per leaf: lane k of a group runs
+// numpy's accumulator r_k (a[k], then += a[8i + k]) -- the eight chains are
+// independent in np_leaf_sum -- and the group combines them by shuffles in
+// numpy's order ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)); the group's
+// first lane adds the n % 8 remainder (or sums a leaf of < 8 sequentially).
+// Bit-identical to np_leaf_sum, with coalesced 64-byte loads per group.
+__device__ void warp_leaf_sums(NormWarpSmem& m, const double* a, uint32_t nleaves, uint32_t lane) {
+    const uint32_t g = lane >> 3, k = lane & 7u;
+    for (uint32_t base = 0; base < nleaves; base += 4) {
+        const uint32_t leaf = base + g;
+        const bool ok = leaf < nleaves;
+        const uint32_t off = ok ? m.leaf_off[leaf] : 0u;
+        const uint32_t len = ok ? m.leaf_len[leaf] : 0u;
+        const double* p = a + off;
+        const uint32_t full = len - len % 8u;
+        double r = 0.0;
+        if (len >= 8) {  // the chain's <= 16 loads issued together, then the adds in order
+            double v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = 8u * i < full ? p[8 * i + k] : 0.0;
+            r = v[0];
+#pragma unroll
+            for (int i = 1; i < 16; ++i)
+                if (8u * i < full) r = __dadd_rn(r, v[i]);
+        }
+        const double t = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));  // k even: r_k + r_k+1
+        const double u = __dadd_rn(t, __shfl_down_sync(0xffffffffu, t, 2));  // k % 4 == 0
+        const double v = __dadd_rn(u, __shfl_down_sync(0xffffffffu, u, 4));  // k == 0
+        if (ok && k == 0) {
+            double res = len >= 8 ? v : 0.0;
+            for (uint32_t i = full; i < len; ++i) res = __dadd_rn(res, p[i]);
+            m.val[leaf] = res;
+        }
     }
+}
+
+__device__ double warp_pairwise_sum(NormWarpSmem& m, const NormTree& t, const double* a, uint64_t n,
+                                    uint32_t lane) {
     double r = 0.0;
-    if (lane == 0) r = combine_leaves(m, n, a, listed);
+    if (t.listed) {
+        warp_leaf_sums(m, a, t.nleaves, lane);
+        __syncwarp();
+        for (int d = (int)t.maxdepth; d >= 0 && t.nnodes; --d) {  // deepest internal nodes first
+            for (uint32_t i = lane; i < t.nnodes; i += 32)
+                if (m.depth[i] == (uint32_t)d)
+                    m.val[kNormMaxLeaves + i] = __dadd_rn(m.val[m.child[i][0]], m.val[m.child[i][1]]);
+            __syncwarp();
+        }
+        r = t.nnodes ? m.val[kNormMaxLeaves] : m.val[0];
+    } else if (lane == 0) {
+        r = combine_serial(m, n, a);
+    }
     __syncwarp();
     return __shfl_sync(0xffffffffu, r, 0);
 }
@@ -201,19 +268,31 @@ __global__ void __launch_bounds__(32 * kNormWarps)
         return;
     }
     double* a = hit_amount + pt.hit_offset;
-    uint32_t nleaves = lane == 0 ? list_leaves(m, pt.hits) : 0;
-    nleaves = __shfl_sync(0xffffffffu, nleaves, 0);
+    NormTree t{};
+    if (lane == 0) t = build_tree(m, pt.hits);
+    t.nleaves = __shfl_sync(0xffffffffu, t.nleaves, 0);
+    t.nnodes = __shfl_sync(0xffffffffu, t.nnodes, 0);
+    t.maxdepth = __shfl_sync(0xffffffffu, t.maxdepth, 0);
+    t.listed = t.nleaves <= (uint32_t)kNormMaxLeaves;
     __syncwarp();
-    const double raw_sum = warp_pairwise_sum(m, a, pt.hits, nleaves, lane);
+    const double raw_sum = warp_pairwise_sum(m, t, a, pt.hits, lane);
     if (raw_sum > 0.0) {
         const double scale = pt.target / raw_sum;
-        for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = __dmul_rn(a[j], scale);
+        uint32_t j = lane;
+        for (; j + 7 * 32 < pt.hits; j += 8 * 32) {  // eight loads in flight per lane
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = a[j + q * 32];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) a[j + q * 32] = __dmul_rn(v[q], scale);
+        }
+        for (; j < pt.hits; j += 32) a[j] = __dmul_rn(a[j], scale);
     } else {
         const double each = pt.target / (double)pt.hits;  // np.full(m, target / m)
         for (uint32_t j = lane; j < pt.hits; j += 32) a[j] = each;
     }
     __syncwarp();
-    const double sum = warp_pairwise_sum(m, a, pt.hits, nleaves, lane);
+    const double sum = warp_pairwise_sum(m, t, a, pt.hits, lane);
     if (lane == 0) particle_sums[p] = sum;
 }
 

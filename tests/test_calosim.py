@@ -163,3 +163,48 @@ def test_gpu_chunking_does_not_change_results(golden, golden_arrays, label):
         assert r["hits"] == r0["hits"] and r["allocated"] == r0["allocated"]
     with pytest.raises(P.InvalidParameter):
         C.simulate_events([[C.Particle("muon", 1.0, (0.0, 0.0, 1.0))]], det, st)
+
+
+@pytest.mark.gpu
+def test_gpu_pairwise_normalisation_all_tree_shapes():
+    """Particles from < 8 hits (one short leaf) through one full leaf, a few
+    leaves, and trees too large for the listed path (> 256 leaves: lane 0
+    sums them on the fly) -- GPU simulate_events against the CPU oracle's
+    simulate_event restatement on the same oracle-generated batches: particle
+    sums (numpy pairwise, bit for bit) and deposits."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2109_01329_b200 as P
+    from oracle import calo_cpu
+
+    nreg = 4
+    geom = [np.arange(r, 4000, nreg, dtype=np.int64) for r in range(nreg)]
+    edges = np.linspace(0.001, 0.101, 9)
+    weights = np.asarray([0.05, 0.10, 0.20, 0.25, 0.20, 0.10, 0.07, 0.03])
+    ranges = {"tiny": (1, 7), "leaf": (8, 128), "few": (129, 700), "huge": (33000, 40000)}
+    det = C.Detector(geom, {k: C.Parameterization(k, lo, hi, edges, weights) for k, (lo, hi) in ranges.items()})
+    rng = np.random.default_rng(3)
+    kinds = list(ranges)
+    events = []
+    for e in range(12):
+        parts = [C.Particle(kinds[(e + j) % 4], float(rng.uniform(1.0, 50.0)),
+                            tuple(rng.normal(size=3) / np.sqrt(3))) for j in range(1 + e % 3)]
+        events.append(parts)
+    min_batch, sf = 1000, 0.8
+    st = P.seed_engine(P.EngineKind.PHILOX4X32X10, 777)
+    final, results = C.simulate_events(events, det, st, min_batch, sf)
+    key = O.seed_philox(777)
+    pp = []
+    hits, allocs = C.plan_from_controls(0, [[ranges[p.kind] for p in ev] for ev in events], min_batch,
+                                        *_oracle_draws(key), per_particle=pp)
+    params = {k: (edges, weights) for k in ranges}
+    pos = 0
+    for e, ev in enumerate(events):
+        batch = O.words_to_unit(O.philox_words(key, pos, allocs[e]), "fp32")
+        dep, psums = calo_cpu.deposit_event(batch, [(p.kind, p.energy, p.direction) for p in ev], pp[e], geom,
+                                            params, nreg, sf)
+        assert results[e].hits == hits[e] and results[e].particle_sums == psums, e
+        assert results[e].deposits == dep, e
+        pos += allocs[e]
+    assert P.stream_position(final) == pos
