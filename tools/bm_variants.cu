@@ -424,6 +424,9 @@ int main(int argc, char** argv) {
     run<1, 12, 1, 2, 5, 256>("ltab, ctr12 quad, loop2 minb5");
     run<1, 12, 1, 0, 4, 256>("ltab, ctr12 quad, loop0 minb4");
     run<1, 13, 0, 2, 0, 512>("ltab, ctr13, loop2 512");
+    run<1, 12, 0, 2, 0, 256>("ltab, ctr12, loop2");
+    run<1, 12, 0, 2, 5, 256>("ltab, ctr12, loop2 minb5");
+    run<1, 12, 0, 0, 4, 256>("ltab, ctr12, loop0 minb4");
     CK(cudaFree(g_out));
     return 0;
 }
