@@ -198,8 +198,11 @@ int prng_calo_hits(const float *batch, const prng_calo_particle_t *particles, ui
  * np.bincount), packed over all events: event e's deposits are
  * dep_cell/dep_energy[dep_offsets[e] .. dep_offsets[e+1]) (dep_offsets has
  * nevents + 1 entries; dep_offsets[nevents] = total deposits <= total_hits).
- * cell_bits: every cell id is < 2^cell_bits (0 = 32); ids < 2^18 are ranked
- * in one shared-memory bitmap window per event, wider ranges in several.
+ * cell_bits: a bound on the cell ids (< 2^cell_bits; 0 = none): ids < 2^18
+ * are ranked in one shared-memory bitmap window per event from 0, wider
+ * ranges in several windows over the event's min/max; an id at or above an
+ * understated bound is detected and its event redone the wide way, so the
+ * result never depends on it.
  * scratch: prng_calo_deposit_scratch_bytes(total_hits, nevents) bytes of
  * device memory (look-back state, zeroed by the call on `stream`, and the
  * bucket arrays of events with more than 8192 hits).  One kernel launch. */

@@ -333,6 +333,7 @@ struct DepSmem {
     uint32_t red[2 * kDepWarps];
     uint32_t scan[kDepWarps];
     uint32_t event, nbig;
+    uint32_t outside;  // a hit outside the window was seen (dep_build_window)
     unsigned long long off;
     uint32_t rbase[(1u << kDepMaxWinLog2) / 64 / kDepRankBlock];
     uint32_t big[kDepCap / (kDepSmall + 1) + 1];  // slots with large buckets (shared-memory path)
@@ -400,13 +401,18 @@ __device__ uint32_t dep_build_window(DepSmem& s, unsigned long long* bm, uint16_
                                      const uint32_t* __restrict__ cells, uint64_t beg, uint64_t end, uint32_t lo,
                                      uint32_t nw) {
     for (uint32_t q = threadIdx.x; q < nw; q += kDepThreads) bm[q] = 0ull;
+    if (threadIdx.x == 0) s.outside = 0u;
     __syncthreads();
     const uint64_t span = 64ull * nw;
+    bool outside = false;
     for (uint64_t i = beg + threadIdx.x; i < end; i += kDepThreads) {
         const uint32_t c = cells[i];
         if (c >= lo && (uint64_t)(c - lo) < span)  // 32-bit halves of the 64-bit words (little-endian)
             atomicOr(reinterpret_cast<unsigned int*>(bm) + ((c - lo) >> 5), 1u << ((c - lo) & 31u));
+        else
+            outside = true;
     }
+    if (outside) s.outside = 1u;
     __syncthreads();
     const uint32_t per = (nw + kDepThreads - 1) / kDepThreads;
     const uint32_t q0 = min(threadIdx.x * per, nw), q1 = min(q0 + per, nw);
@@ -603,26 +609,37 @@ __global__ void __launch_bounds__(kDepThreads, 3)
         const uint32_t e = s.event;
         if (e >= nevents) return;
         const uint64_t beg = ev_off[e], end = ev_off[e + 1];
-        uint32_t lo = 0, cmax = (uint32_t)(win - 1);  // ids < 2^wbits: one window from 0, no min/max pass
-        if (end > beg && wide) dep_minmax(s, cells, beg, end, 0, lo, cmax);
+        // ids < 2^cell_bits <= 2^wbits: one window from 0, no min/max pass --
+        // unless a hit outside it shows cell_bits understated the ids, then the
+        // event is redone with min/max and windows (results do not depend on it)
+        bool ev_wide = wide;
+        uint32_t lo = 0, cmax = (uint32_t)(win - 1);
+        uint64_t total = 0;
+        uint32_t first_u = 0;
+        bool single = true;
         auto words_of = [&](uint32_t wlo) {  // words covering [wlo, min(cmax, wlo + win - 1)]
             const uint64_t top = (uint64_t)cmax - wlo;
             return top >= win ? nwords : (uint32_t)(top >> 6) + 1u;
         };
-        const bool single = end == beg || (uint64_t)cmax - lo < win;
         // 1. count (a single window stays built for step 3)
-        uint64_t total = 0;
-        uint32_t first_u = 0;
-        if (end > beg) {
-            uint32_t wlo = lo;
-            for (;;) {
-                const uint32_t u = dep_build_window(s, bm, pref, cells, beg, end, wlo, words_of(wlo));
-                if (wlo == lo) first_u = u;
-                total += u;
-                if (single || (uint64_t)wlo + win > cmax) break;
-                uint32_t unused;
-                dep_minmax(s, cells, beg, end, (uint64_t)wlo + win, wlo, unused);  // exists: cmax qualifies
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            if (end > beg && ev_wide) dep_minmax(s, cells, beg, end, 0, lo, cmax);
+            single = end == beg || (uint64_t)cmax - lo < win;
+            total = 0;
+            if (end > beg) {
+                uint32_t wlo = lo;
+                for (;;) {
+                    const uint32_t u = dep_build_window(s, bm, pref, cells, beg, end, wlo, words_of(wlo));
+                    if (wlo == lo) first_u = u;
+                    total += u;
+                    if (single || (uint64_t)wlo + win > cmax) break;
+                    uint32_t unused;
+                    dep_minmax(s, cells, beg, end, (uint64_t)wlo + win, wlo, unused);  // exists: cmax qualifies
+                }
             }
+            if (ev_wide || end == beg || !s.outside) break;
+            ev_wide = true;  // an id >= 2^wbits: redo with min/max
+            __syncthreads();
         }
         // 2. packed offset: decoupled look-back over the earlier events
         if (threadIdx.x == 0) {

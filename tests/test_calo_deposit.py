@@ -146,3 +146,27 @@ def test_deposit_narrow_ids_and_bucket_storage():
         assert np.array_equal(np.diff(got_o), counts)
         assert np.array_equal(got_c, want_c)
         assert np.array_equal(got_e.view(np.uint64), want_e.view(np.uint64))
+
+
+def test_deposit_understated_cell_bits_is_detected():
+    """cell_bits is a performance hint: ids at or above 2^cell_bits (an
+    understated bound) are detected per event and the event is redone over
+    min/max windows, so the deposits are still numpy's."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2109_01329_b200 import _lib
+    rng = np.random.default_rng(17)
+    ev = [(rng.integers(0, 1 << 10, 500).astype(np.uint32), rng.random(500)),        # inside 2^10
+          (rng.integers(0, 1 << 18, 3000).astype(np.uint32), rng.random(3000)),      # mostly outside
+          (np.array([1023, 1024, 5, 1 << 31], np.uint32), rng.random(4)),            # straddles, and far
+          (np.zeros(0, np.uint32), np.zeros(0))]
+    cells = np.concatenate([c for c, _ in ev]).astype(np.uint32)
+    amts = np.concatenate([a for _, a in ev]).astype(np.float64)
+    offs = np.zeros(len(ev) + 1, dtype=np.int64)
+    np.cumsum([len(c) for c, _ in ev], out=offs[1:])
+    want_c, want_e, counts = _numpy_deposits(cells, amts, offs)
+    got_c, got_e, got_o = _run(_lib.lib, torch, cells, amts, offs, 10)
+    assert np.array_equal(np.diff(got_o), counts)
+    assert np.array_equal(got_c, want_c)
+    assert np.array_equal(got_e.view(np.uint64), want_e.view(np.uint64))
