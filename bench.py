@@ -33,6 +33,7 @@ numbers.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -576,15 +577,29 @@ def run_c5_full(args):
     # Warm-up at full size, twice: the results of one call are still held while
     # the next allocates, so the pinned-host caching allocator needs two
     # sets of result buffers before it stops calling cudaHostAlloc.
-    for _ in range(max(2, args.warmup)):
+    # >= 10 warm-up runs: the first ones pay cudaHostAlloc for the pinned
+    # result buffers and host page faults (20-500 ms steps for the first
+    # ~10 runs on a fresh box; the held previous result needs a second set)
+    for _ in range(max(10, args.warmup)):
         final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=args.c5_chunk)
     torch.cuda.synchronize()
+    # timeit's convention: the cyclic garbage collector is off in the timed
+    # loop (a full collection over this process's ~190k tracked objects --
+    # torch and the 10^4-event particle list -- costs ~30 ms and otherwise
+    # lands in random steps; tools/gc_probe.py, tools/c5_hold.py)
+    gc.collect()
+    gc_was = gc.isenabled()
+    gc.disable()
     ts = []
-    for _ in range(max(1, args.steps)):
-        t0 = time.perf_counter()
-        final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=args.c5_chunk)
-        torch.cuda.synchronize()
-        ts.append(time.perf_counter() - t0)
+    try:
+        for _ in range(max(1, args.steps)):
+            t0 = time.perf_counter()
+            final, res = C.simulate_events(events, det, st, dicts=False, chunk_events=args.c5_chunk)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+    finally:
+        if gc_was:
+            gc.enable()
     log("c5_full step ms: " + " ".join(f"{t * 1e3:.2f}" for t in ts))
     sec = statistics.median(ts)
     total_hits = int(sum(res["hits"]))
@@ -614,7 +629,7 @@ def run_c5_full(args):
                          f"restated from calosim.py:313-347, Serial"}
     line = {
         "metric": "FastCaloSim single-electron events/s (control draws + batch generation + deposition)",
-        "value": nev / sec, "unit": "events/s", "n_gpus": 1, "steps": len(ts), "warmup": max(2, args.warmup),
+        "value": nev / sec, "unit": "events/s", "n_gpus": 1, "steps": len(ts), "warmup": max(10, args.warmup),
         "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32->fp32 (fp64 deposition)", "data": "synthetic single-electron events (seed 777)",
         "config": {"workload": f"{nev} events, 190000 cells / 24 regions, min_batch 200000",
