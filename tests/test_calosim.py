@@ -75,7 +75,7 @@ def test_cpu_deposition_oracle_matches_reference(golden, golden_arrays, label):
 @pytest.mark.parametrize("label", ["electron", "ttbar_small_batch"])
 def test_gpu_deposition_bit_identical_to_reference(golden, golden_arrays, label):
     """simulate_events (control draws, one segment launch, hit kernel,
-    pairwise normalisation, segmented sort + run sums) == the reference's
+    pairwise normalisation, deposit kernel) == the reference's
     simulate_event deposits, particle sums and accounting, exactly."""
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
