@@ -701,6 +701,33 @@ int calo_fail(int code, const char* fmt, ...) {
     va_end(ap);
     return prng_detail_fail(code, buf);
 }
+
+// The device that owns `ptr` is current for the entry point; the caller's
+// device is restored on return (as for the generator entry points, api.cu).
+struct CaloDevice {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit CaloDevice(const void* ptr) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        cudaPointerAttributes attr;
+        err = cudaPointerGetAttributes(&attr, ptr);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        if ((attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) && attr.device != prev)
+            err = cudaSetDevice(attr.device);
+    }
+    ~CaloDevice() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    CaloDevice(const CaloDevice&) = delete;
+    CaloDevice& operator=(const CaloDevice&) = delete;
+};
 }  // namespace
 
 extern "C" {
@@ -712,6 +739,8 @@ int prng_calo_hits(const float* batch, const prng_calo_particle_t* particles, ui
     if (!batch || !particles || !region_offsets || !region_cells || !params || !hit_cell || !hit_amount ||
         !particle_sums)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "NULL argument");
+    const CaloDevice on(hit_amount);
+    if (on.err != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "calo hits: %s", cudaGetErrorString(on.err));
     cudaStream_t s = (cudaStream_t)stream;
     calo_hits_kernel<<<nparticles, kCaloThreads, 0, s>>>(batch, particles, region_offsets, region_cells, params,
                                                          hit_cell, hit_amount);
@@ -746,6 +775,8 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     const size_t need = deposit_scratch(total_hits, nevents);
     if (!scratch || scratch_bytes < need)
         return calo_fail(PRNG_ERR_INVALID_PARAMETER, "scratch too small: need %zu bytes", need);
+    const CaloDevice on(dep_energy);
+    if (on.err != cudaSuccess) return calo_fail(PRNG_ERR_CUDA, "calo deposit: %s", cudaGetErrorString(on.err));
     cudaStream_t s = (cudaStream_t)stream;
     // bitmap window: the whole cell-id range when it has <= 2^18 ids
     const uint32_t b = cell_bits == 0 ? 32u : cell_bits;
