@@ -20,6 +20,7 @@
 #include <cuda/atomic>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 
@@ -318,7 +319,9 @@ __global__ void __launch_bounds__(32 * kNormWarps)
 //     sequential one, bit for bit;
 //  4. the sums and the cells are written packed at the event's offset.
 // Events of up to 8192 hits keep their counters and indices in shared
-// memory (16-bit), larger ones in the caller's scratch (32-bit).  A cell
+// memory (16-bit; each thread's <= 32 slots stay in registers from the count
+// to the fill, so the bucket indices overwrite the no longer needed bitmap:
+// 56 KB, 4 CTAs per SM), larger ones in the caller's scratch (32-bit).  A cell
 // range wider than the window is covered by successive windows, each
 // starting at the smallest cell not yet covered.
 constexpr int kDepThreads = 256;
@@ -327,6 +330,9 @@ constexpr uint32_t kDepMaxWinLog2 = 18;  // 2^18 cells: 32 KB bitmap + 8 KB of 1
 constexpr uint32_t kDepRankBlock = 256;  // words per 32-bit rank base
 constexpr uint32_t kDepCap = 8192;       // hits per event indexed in shared memory
 constexpr uint32_t kDepSmall = 32;       // larger buckets are ordered by the whole CTA
+#ifndef PRNG_DEP_ALIAS  // 1: the shared-memory buckets overwrite the bitmap after the count (56 KB, 4 CTAs/SM)
+#define PRNG_DEP_ALIAS 1
+#endif
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
 
 struct DepSmem {
@@ -439,6 +445,7 @@ __device__ __forceinline__ uint32_t dep_rank(const DepSmem& s, const unsigned lo
 // Bucket storage.  Shared memory: 16-bit counters packed in pairs and 16-bit
 // hit indices; global (events of more than kDepCap hits): 32-bit, in scratch.
 struct DepIdxShared {
+    static constexpr bool kRegSlots = PRNG_DEP_ALIAS != 0;  // lst aliases the bitmap (see the kernel)
     uint32_t* cnt2;
     uint16_t* lst;
     uint32_t* big;
@@ -470,6 +477,7 @@ struct DepIdxShared {
 };
 
 struct DepIdxGlobal {
+    static constexpr bool kRegSlots = false;
     uint32_t* cnt;
     uint32_t* lst;
     uint32_t* big;
@@ -525,16 +533,41 @@ __device__ void dep_window(DepSmem& s, const IX& ix, const unsigned long long* b
     ix.zero(u);
     if (threadIdx.x == 0) s.nbig = 0;
     __syncthreads();
-    for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
-        const uint32_t c = cells[beg + h];
-        if (c >= lo && (uint64_t)(c - lo) < span) ix.add(dep_rank(s, bm, pref, c - lo));
-    }
-    __syncthreads();
-    ix.scan(s, u);
-    __syncthreads();
-    for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
-        const uint32_t c = cells[beg + h];
-        if (c >= lo && (uint64_t)(c - lo) < span) ix.put(ix.add(dep_rank(s, bm, pref, c - lo)), h);
+    if constexpr (IX::kRegSlots) {
+        // <= 32 hits per thread: their slots (16 bits, 0xFFFF = outside the
+        // window) stay in registers from the count to the fill, so the fill
+        // needs no ranks and its buckets may overwrite the bitmap
+        uint32_t sl2[kDepCap / kDepThreads / 2];
+#pragma unroll
+        for (int j = 0; j < (int)(kDepCap / kDepThreads); ++j) {
+            const uint32_t h = threadIdx.x + j * kDepThreads;
+            uint32_t sl = 0xFFFFu;
+            if (h < nh) {
+                const uint32_t c = cells[beg + h];
+                if (c >= lo && (uint64_t)(c - lo) < span) ix.add(sl = dep_rank(s, bm, pref, c - lo));
+            }
+            if (j & 1) sl2[j / 2] |= sl << 16; else sl2[j / 2] = sl;
+        }
+        __syncthreads();
+        ix.scan(s, u);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < (int)(kDepCap / kDepThreads); ++j) {
+            const uint32_t sl = (sl2[j / 2] >> ((j & 1) * 16)) & 0xFFFFu;
+            if (sl != 0xFFFFu) ix.put(ix.add(sl), threadIdx.x + j * kDepThreads);
+        }
+    } else {
+        for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
+            const uint32_t c = cells[beg + h];
+            if (c >= lo && (uint64_t)(c - lo) < span) ix.add(dep_rank(s, bm, pref, c - lo));
+        }
+        __syncthreads();
+        ix.scan(s, u);
+        __syncthreads();
+        for (uint32_t h = threadIdx.x; h < nh; h += kDepThreads) {
+            const uint32_t c = cells[beg + h];
+            if (c >= lo && (uint64_t)(c - lo) < span) ix.put(ix.add(dep_rank(s, bm, pref, c - lo)), h);
+        }
     }
     __syncthreads();
     // counters now hold each bucket's end; bucket sl = [end(sl - 1), end(sl))
@@ -588,7 +621,7 @@ __device__ void dep_window(DepSmem& s, const IX& ix, const unsigned long long* b
     }
 }
 
-__global__ void __launch_bounds__(kDepThreads, 3)
+__global__ void __launch_bounds__(kDepThreads, PRNG_DEP_ALIAS ? 4 : 3)
     calo_deposit_kernel(const uint32_t* __restrict__ cells, const double* __restrict__ amts,
                         const uint64_t* __restrict__ ev_off, uint32_t nevents, uint32_t cell_bits, uint32_t wbits,
                         unsigned long long* status, unsigned int* ticket, uint32_t* gidx, uint64_t total_hits,
@@ -598,9 +631,16 @@ __global__ void __launch_bounds__(kDepThreads, 3)
     __shared__ DepSmem s;
     const uint32_t nwords = 1u << (wbits - 6);
     unsigned long long* bm = reinterpret_cast<unsigned long long*>(dep_dyn);
+#if PRNG_DEP_ALIAS
+    const uint32_t region = max(nwords * 8u, kDepCap * 2u);  // bitmap, then the buckets
+    uint16_t* lst = reinterpret_cast<uint16_t*>(dep_dyn);
+    uint32_t* cnt2 = reinterpret_cast<uint32_t*>(dep_dyn + region);
+    uint16_t* pref = reinterpret_cast<uint16_t*>(cnt2 + kDepCap / 2);
+#else
     uint32_t* cnt2 = reinterpret_cast<uint32_t*>(bm + nwords);
     uint16_t* lst = reinterpret_cast<uint16_t*>(cnt2 + kDepCap / 2);
     uint16_t* pref = lst + kDepCap;
+#endif
     const uint64_t win = 64ull * nwords;
     const bool wide = cell_bits == 0 || cell_bits > wbits;  // ids may lie beyond the first window
     for (;;) {
@@ -782,8 +822,13 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     const uint32_t b = cell_bits == 0 ? 32u : cell_bits;
     const uint32_t wbits = b < 6u ? 6u : (b > kDepMaxWinLog2 ? kDepMaxWinLog2 : b);
     const uint32_t nwords = 1u << (wbits - 6);
+#if PRNG_DEP_ALIAS
+    const size_t smem = std::max<size_t>((size_t)nwords * sizeof(unsigned long long), kDepCap * sizeof(uint16_t)) +
+                        kDepCap / 2 * sizeof(uint32_t) + (size_t)nwords * sizeof(uint16_t);
+#else
     const size_t smem = (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint16_t)) +
                         kDepCap / 2 * sizeof(uint32_t) + kDepCap * sizeof(uint16_t);
+#endif
     int dev = 0, nsm = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
