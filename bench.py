@@ -682,8 +682,11 @@ def run_c5(args):
     out = torch.empty(total, dtype=torch.float32, device="cuda")
     dtab = torch.from_numpy(table.view(np.int64).reshape(-1, 4).copy()).cuda()
 
+    warm = max(3, args.warmup)
+
     def timed(fn, reps):
-        fn()
+        for _ in range(warm):
+            fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
@@ -725,7 +728,7 @@ def run_c5(args):
                "sample": f"{sample} events x 200000 fp32 uniforms, per-event generate + affine (Serial)"}
     line = {
         "metric": "Gsamples/s of FastCaloSim-style per-event uniform batches (C5)", "value": value,
-        "unit": "Gsamples/s", "n_gpus": 1, "steps": args.steps, "warmup": 1,
+        "unit": "Gsamples/s", "n_gpus": 1, "steps": args.steps, "warmup": warm,
         "ms_per_step": modes[best], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "u32->fp32", "data": "synthetic single-electron events (seed 777)",
         "config": {"workload": f"{nev} events x max(3*hits,200000) fp32 uniforms at chained offsets",
