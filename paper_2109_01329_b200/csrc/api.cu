@@ -501,14 +501,9 @@ int launch_philox(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t lane, 
     int sms = 0, occ = 0;
     rc = resident_ctas(kern, kPhiloxThreads, &sms, &occ);
     if (rc) return rc;
-#ifndef PRNG_GRID_MULT
-#define PRNG_GRID_MULT 1
-#endif
-#ifndef PRNG_SMALLN_NOCAP_LOG2  // requests of < 2^this groups: one pass per thread (no persistent cap)
-#define PRNG_SMALLN_NOCAP_LOG2 0
-#endif
-    uint64_t cap = (uint64_t)sms * occ * PRNG_GRID_MULT;
-    if (ngroups < (1ull << PRNG_SMALLN_NOCAP_LOG2)) cap = ~0ull >> 1;
+    // persistent grid: every SM filled to the kernel's occupancy (2x / 4x and
+    // uncapped grids measured no faster at 2^22-2^26, profiles/r2_ab_small_n_grid.txt)
+    const uint64_t cap = (uint64_t)sms * occ;
 
     u128 blk = (((u128)s.ctr_hi << 64) | s.ctr_lo) + ((lane + i0) >> 2);
     T* body = static_cast<T*>(dptr) + i0;
