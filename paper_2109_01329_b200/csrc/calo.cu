@@ -330,9 +330,6 @@ constexpr uint32_t kDepMaxWinLog2 = 18;  // 2^18 cells: 32 KB bitmap + 8 KB of 1
 constexpr uint32_t kDepRankBlock = 256;  // words per 32-bit rank base
 constexpr uint32_t kDepCap = 8192;       // hits per event indexed in shared memory
 constexpr uint32_t kDepSmall = 32;       // larger buckets are ordered by the whole CTA
-#ifndef PRNG_DEP_ALIAS  // 1: the shared-memory buckets overwrite the bitmap after the count (56 KB, 4 CTAs/SM)
-#define PRNG_DEP_ALIAS 1
-#endif
 constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
 
 struct DepSmem {
@@ -445,7 +442,7 @@ __device__ __forceinline__ uint32_t dep_rank(const DepSmem& s, const unsigned lo
 // Bucket storage.  Shared memory: 16-bit counters packed in pairs and 16-bit
 // hit indices; global (events of more than kDepCap hits): 32-bit, in scratch.
 struct DepIdxShared {
-    static constexpr bool kRegSlots = PRNG_DEP_ALIAS != 0;  // lst aliases the bitmap (see the kernel)
+    static constexpr bool kRegSlots = true;  // slots in registers from count to fill: lst may alias the bitmap
     uint32_t* cnt2;
     uint16_t* lst;
     uint32_t* big;
@@ -621,7 +618,7 @@ __device__ void dep_window(DepSmem& s, const IX& ix, const unsigned long long* b
     }
 }
 
-__global__ void __launch_bounds__(kDepThreads, PRNG_DEP_ALIAS ? 4 : 3)
+__global__ void __launch_bounds__(kDepThreads, 4)
     calo_deposit_kernel(const uint32_t* __restrict__ cells, const double* __restrict__ amts,
                         const uint64_t* __restrict__ ev_off, uint32_t nevents, uint32_t cell_bits, uint32_t wbits,
                         unsigned long long* status, unsigned int* ticket, uint32_t* gidx, uint64_t total_hits,
@@ -631,16 +628,12 @@ __global__ void __launch_bounds__(kDepThreads, PRNG_DEP_ALIAS ? 4 : 3)
     __shared__ DepSmem s;
     const uint32_t nwords = 1u << (wbits - 6);
     unsigned long long* bm = reinterpret_cast<unsigned long long*>(dep_dyn);
-#if PRNG_DEP_ALIAS
-    const uint32_t region = max(nwords * 8u, kDepCap * 2u);  // bitmap, then the buckets
+    // the bitmap, overwritten by the 16-bit bucket indices once the count
+    // has put every hit's slot in registers; then the counters and word ranks
+    const uint32_t region = max(nwords * 8u, kDepCap * 2u);
     uint16_t* lst = reinterpret_cast<uint16_t*>(dep_dyn);
     uint32_t* cnt2 = reinterpret_cast<uint32_t*>(dep_dyn + region);
     uint16_t* pref = reinterpret_cast<uint16_t*>(cnt2 + kDepCap / 2);
-#else
-    uint32_t* cnt2 = reinterpret_cast<uint32_t*>(bm + nwords);
-    uint16_t* lst = reinterpret_cast<uint16_t*>(cnt2 + kDepCap / 2);
-    uint16_t* pref = lst + kDepCap;
-#endif
     const uint64_t win = 64ull * nwords;
     const bool wide = cell_bits == 0 || cell_bits > wbits;  // ids may lie beyond the first window
     for (;;) {
@@ -822,13 +815,8 @@ int prng_calo_deposit(const uint32_t* hit_cell, const double* hit_amount, uint64
     const uint32_t b = cell_bits == 0 ? 32u : cell_bits;
     const uint32_t wbits = b < 6u ? 6u : (b > kDepMaxWinLog2 ? kDepMaxWinLog2 : b);
     const uint32_t nwords = 1u << (wbits - 6);
-#if PRNG_DEP_ALIAS
     const size_t smem = std::max<size_t>((size_t)nwords * sizeof(unsigned long long), kDepCap * sizeof(uint16_t)) +
-                        kDepCap / 2 * sizeof(uint32_t) + (size_t)nwords * sizeof(uint16_t);
-#else
-    const size_t smem = (size_t)nwords * (sizeof(unsigned long long) + sizeof(uint16_t)) +
-                        kDepCap / 2 * sizeof(uint32_t) + kDepCap * sizeof(uint16_t);
-#endif
+                        kDepCap / 2 * sizeof(uint32_t) + (size_t)nwords * sizeof(uint16_t);  // 56 KB at 2^18
     int dev = 0, nsm = 0, per_sm = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
